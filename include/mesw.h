@@ -1,0 +1,181 @@
+/*
+ * mesw.h -- C ABI of the B200-native ME-Switch multi-expert serving hot path.
+ *
+ * The reference (arXiv 2406.09041, /root/reference/pkg/src/meswitch) is pure
+ * Python/numpy and has no FFI of its own.  This header is the boundary the
+ * reference would bind (ctypes) to move its hot path to
+ * the GPU.  Each entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "d_" pointers are CUDA device pointers,
+ *    "h_" pointers are host pointers.  `stream` is a cudaStream_t (NULL = legacy
+ *    default stream).
+ *  - Every function returns a mesw_status.  No C++ exception crosses the ABI;
+ *    mesw_last_error() returns a thread-local message for the last failure.
+ *  - Matrix orientation follows the reference (numerics.py:1-8): a delta /
+ *    weight is [m x n] with rows = INPUT channels, columns = OUTPUT channels,
+ *    y = x . W.
+ *
+ * Device layouts: a linear with m inputs
+ * and n outputs is padded to m_pad = ceil(m/128)*128, n_pad = ceil(n/128)*128
+ * and cut into column groups (cg, 128 outputs) x k-steps (ks, 128 inputs).
+ *  - base weight  : bf16, [cg][ks][tile 8][kblock 8][lane 32][8 elems]
+ *                   (one mma.m16n8k16 A fragment per lane per k-block; 32 KiB per (cg,ks))
+ *  - delta codes  : DB-bit device codes d = q + OFF (DB=2: b=2, OFF=2; DB=4:
+ *                   b in {1,3,4}, OFF=8; DB=8: b=8, OFF=128), [cg][ks][tile][lane][8*DB bytes];
+ *                   salient input rows forced to d = OFF (q = 0), which keeps the fused
+ *                   result equal to CompressedDelta.reconstruct() (compress.py:115-121)
+ *  - steps        : f32 [n_pad]
+ *  - salient      : per column group: sal_off[n_cg+1] (int32), sal_idx[] (int32 input
+ *                   channel), sal_rows[][128] (binary16 bits of R restricted to the cg)
+ */
+#ifndef MESW_H_
+#define MESW_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MESW_OK = 0,
+  MESW_ERR_BAD_MAGIC = 1,           /* errors.BadMagicError          (errors.py:23) */
+  MESW_ERR_UNSUPPORTED_VERSION = 2, /* errors.UnsupportedVersionError(errors.py:27) */
+  MESW_ERR_TRUNCATED = 3,           /* errors.TruncatedArtifactError (errors.py:31) */
+  MESW_ERR_VALUE = 4,               /* ValueError (shape / range / bits)            */
+  MESW_ERR_CUDA = 5,                /* CUDA runtime failure                          */
+  MESW_ERR_UNSUPPORTED = 6          /* valid input this build does not handle        */
+} mesw_status;
+
+#define MESW_TILE_N 128 /* outputs per column group  */
+#define MESW_TILE_K 128 /* inputs per k-step         */
+#define MESW_MAX_SEGMENTS 64
+
+/* ---------------------------------------------------------------- misc */
+int mesw_abi_version(void);
+const char* mesw_last_error(void);
+/* Number of SMs of the current device (grid sizing), or -1. */
+int mesw_device_sm_count(void);
+
+/* --------------------------------------------- MESW container (host side)
+ * Replaces compress.deserialize_artifact (compress.py:513-549): validates the
+ * magic, version, every layer block and the absence of trailing bytes, and
+ * returns byte offsets of each block's fields into `buf` (no copies).       */
+typedef struct {
+  uint32_t m, n, bits, k;
+  uint64_t idx_off;   /* k x u32 salient input channels, ascending            */
+  uint64_t rows_off;  /* k x n x u16 binary16 salient rows                     */
+  uint64_t steps_off; /* n x f32 step sizes                                    */
+  uint64_t codes_off; /* packed codes, column-major LSB-first (quant.py:172-213) */
+  uint64_t codes_len;
+} mesw_layer_view;
+
+/* Parse the container header: manifest JSON at [*manifest_off, +*manifest_len). */
+int mesw_parse_header(const uint8_t* h_buf, uint64_t len, uint64_t* manifest_off,
+                      uint32_t* manifest_len);
+/* Walk `layer_count` layer blocks starting at `first_off`; fills `views`. */
+int mesw_parse_layers(const uint8_t* h_buf, uint64_t len, uint64_t first_off,
+                      uint32_t layer_count, mesw_layer_view* views);
+/* quant.packed_nbytes (quant.py:190-192). */
+uint64_t mesw_packed_nbytes(uint32_t rows, uint32_t cols, uint32_t bits);
+/* compress.layer_block_nbytes(...).total (compress.py:589-597). */
+uint64_t mesw_layer_block_nbytes(uint32_t m, uint32_t n, uint32_t bits, uint32_t k);
+
+/* ------------------------------------------------ device geometry / loader */
+/* Device code width for a MESW bit width: 2 -> 2, {1,3,4} -> 4, 8 -> 8 (0 if invalid). */
+int mesw_device_code_bits(uint32_t bits);
+/* Bytes of the device code buffer / base weight buffer for a padded linear. */
+uint64_t mesw_codes_device_bytes(uint32_t m_pad, uint32_t n_pad, uint32_t code_bits);
+uint64_t mesw_weight_device_bytes(uint32_t m_pad, uint32_t n_pad);
+
+/* K1: repack one MESW layer block's packed codes (already on the device,
+ * d_packed = the raw column-major run bytes) into the device code layout of
+ * a (possibly fused) linear, at output-column offset col_base (multiple of
+ * 128).  Salient rows (d_sal_idx, ascending, k entries) are forced to q = 0.
+ * Replaces the consumer side of quant.unpack_codes (quant.py:216-236).       */
+int mesw_repack_codes(const uint8_t* d_packed, uint32_t m, uint32_t n, uint32_t bits,
+                      const int32_t* d_sal_idx, uint32_t k, uint8_t* d_codes,
+                      uint32_t m_pad, uint32_t n_total_pad, uint32_t col_base,
+                      void* stream);
+
+/* Repack a bf16 base weight into the fragment layout.  If `transposed` == 0 the
+ * source is [m][ld] (reference orientation, rows = inputs); otherwise [n][ld]
+ * (torch nn.Linear weight, rows = outputs).  Written at column offset col_base. */
+int mesw_repack_weight(const uint16_t* d_src, uint32_t m, uint32_t n, uint32_t ld,
+                       int transposed, uint16_t* d_w, uint32_t m_pad,
+                       uint32_t n_total_pad, uint32_t col_base, void* stream);
+
+/* Host helper: build the per-column-group salient tables of a fused linear from
+ * its blocks.  Block b covers output columns [col_base[b], col_base[b]+n[b]),
+ * has k[b] salient input channels h_idx[b][...] and rows h_rows[b] (k x n
+ * binary16).  Call once with the out pointers NULL to get *total, then again.  */
+int mesw_build_salient_tables(uint32_t n_blocks, const uint32_t* col_base, const uint32_t* n,
+                              const uint32_t* k, const uint32_t* const* h_idx,
+                              const uint16_t* const* h_rows, uint32_t n_total_pad,
+                              int32_t* h_sal_off, int32_t* h_sal_idx, uint16_t* h_sal_rows,
+                              uint64_t* total);
+
+/* K6 debug: device codes -> int8 codes [m][n] (row-major, reference
+ * orientation) of the block at col_base; bit-exact with quant.unpack_codes
+ * except salient rows, which read 0 (compress.py:205-214 writes them as 0). */
+int mesw_unpack_codes_debug(const uint8_t* d_codes, uint32_t code_bits, uint32_t m,
+                            uint32_t n, uint32_t m_pad, uint32_t n_total_pad,
+                            uint32_t col_base, int8_t* d_out, void* stream);
+/* K6 debug: dense f32 [m][n] reconstruction = CompressedDelta.reconstruct(). */
+int mesw_dequant_debug(const uint8_t* d_codes, uint32_t code_bits, const float* d_steps,
+                       const int32_t* d_sal_off, const int32_t* d_sal_idx,
+                       const uint16_t* d_sal_rows, uint32_t m, uint32_t n, uint32_t m_pad,
+                       uint32_t n_total_pad, uint32_t col_base, float* d_out, void* stream);
+/* Debug: fragment-layout base weight -> bf16 [m][n] (reference orientation). */
+int mesw_unpack_weight_debug(const uint16_t* d_w, uint32_t m, uint32_t n, uint32_t m_pad,
+                             uint32_t n_total_pad, uint32_t col_base, uint16_t* d_out,
+                             void* stream);
+
+/* ------------------------------------------- K2: fused multi-expert linear
+ * y[t, :] = x[t, :] . W  +  x[t, :] . Dtilde_{expert(t)}  (+ residual[t, :])
+ * with Dtilde applied straight from the packed codes (Eq. 4
+ * PAPER.md:123-130): s_j * sum_{i not in S} x_i q_ij + sum_{i in S} x_i half(R)_ij.
+ * Tokens are grouped by expert: segment s covers rows [seg_begin[s], seg_end[s])
+ * and uses expert-table slot seg_slot[s]; rows in no segment get no delta.
+ * Replaces toylm._apply_delta + provider (toylm.py:183-186) and SPEC
+ * delta_matvec / batched_multi_model_forward's shared-base + delta stages.  */
+typedef struct {
+  const void* codes;        /* device code layout of this expert's linear     */
+  const float* steps;       /* [n_pad]                                         */
+  const int32_t* sal_off;   /* [n_cg + 1]                                      */
+  const int32_t* sal_idx;   /* [sal_off[n_cg]]                                 */
+  const uint16_t* sal_rows; /* [sal_off[n_cg]][128] binary16                   */
+} mesw_expert_dev;
+
+typedef struct {
+  const uint16_t* x;  /* bf16 [B][ldx]; columns m..m_pad-1 must be 0          */
+  int32_t B, m, n, ldx;
+  const uint16_t* w;  /* fragment-layout bf16 base, or NULL (delta only)      */
+  const mesw_expert_dev* expert_table; /* DEVICE array indexed by slot        */
+  int32_t code_bits;  /* 2, 4 or 8: shared by all experts of the launch       */
+  int32_t n_segments; /* <= MESW_MAX_SEGMENTS                                 */
+  int32_t seg_begin[MESW_MAX_SEGMENTS];
+  int32_t seg_end[MESW_MAX_SEGMENTS];
+  int32_t seg_slot[MESW_MAX_SEGMENTS];
+  void* y;            /* [B][ldy] output                                       */
+  int32_t y_bf16;     /* 1: bf16 output, 0: f32 output                         */
+  int32_t ldy;
+  const uint16_t* residual; /* optional bf16 [B][ld_res], added before rounding */
+  int32_t ld_res;
+  void* workspace;    /* scratch for split-K partials                          */
+  uint64_t workspace_bytes;
+  int32_t* counters;  /* >= n_pad/128 int32, zero before first use (self-resetting) */
+  int32_t num_ctas;   /* 0 = one persistent CTA per SM                         */
+  int32_t activation; /* 0: none, 1: ReLU (toylm.py:207), applied last         */
+} mesw_linear_args;
+
+/* Workspace bytes mesw_me_linear needs for a given B and CTA count. */
+uint64_t mesw_linear_workspace_bytes(int32_t B, int32_t num_ctas);
+int mesw_me_linear(const mesw_linear_args* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MESW_H_ */

@@ -1,0 +1,339 @@
+"""GPU-resident packed delta format, loader and the fused multi-expert linear call.
+
+Everything here drives the C ABI (include/mesw.h) with device pointers owned by
+torch tensors (torch is only the allocator/stream plumbing).  There is no CPU
+path: every compute call launches a CUDA kernel from libmesw.so.
+
+Layouts: a linear with m inputs and output blocks n_0, n_1, ...
+(fused q|k|v or gate|up) is padded to m_pad = ceil128(m); block b starts at
+output column col_base[b] (multiple of 128).  Each expert's linear owns
+  codes    uint8 [m_pad * n_pad * DB / 8]   fragment-ordered DB-bit codes, d = q + OFF
+  steps    f32   [n_pad]
+  sal_off  int32 [n_pad/128 + 1], sal_idx int32 [*], sal_rows fp16 [*][128]
+and the shared base owns a bf16 fragment-ordered weight [m_pad * n_pad].
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .compress import CompressedDelta
+
+TILE = 128
+
+
+def _ceil(v: int, q: int = TILE) -> int:
+    return (v + q - 1) // q * q
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+@dataclass(frozen=True)
+class LinearGeometry:
+    """Input width m and output blocks of a (possibly fused) linear."""
+
+    m: int
+    block_n: tuple
+
+    @property
+    def m_pad(self) -> int:
+        return _ceil(self.m)
+
+    @property
+    def col_base(self) -> tuple:
+        out, acc = [], 0
+        for nb in self.block_n:
+            out.append(acc)
+            acc += _ceil(nb)
+        return tuple(out)
+
+    @property
+    def n_pad(self) -> int:
+        return sum(_ceil(nb) for nb in self.block_n)
+
+    @property
+    def n(self) -> int:
+        """Output width the kernel writes (up to the end of the last block)."""
+        return self.col_base[-1] + self.block_n[-1]
+
+    @property
+    def n_cg(self) -> int:
+        return self.n_pad // TILE
+
+
+# --------------------------------------------------------------------------- deltas
+
+@dataclass
+class DeviceDelta:
+    """One expert's compressed delta for one (fused) linear, resident in HBM."""
+
+    geom: LinearGeometry
+    bits: int
+    code_bits: int
+    codes: torch.Tensor
+    steps: torch.Tensor
+    sal_off: torch.Tensor
+    sal_idx: torch.Tensor
+    sal_rows: torch.Tensor
+    nbytes: int = 0
+
+    @classmethod
+    def from_blocks(cls, blocks: list, geom: LinearGeometry | None = None, device="cuda",
+                    stream=None) -> "DeviceDelta":
+        """Upload + repack MESW layer blocks (one per output block) into the device layout."""
+        L = _lib.lib()
+        blocks = list(blocks)
+        if geom is None:
+            geom = LinearGeometry(blocks[0].rows, tuple(b.cols for b in blocks))
+        if len(blocks) != len(geom.block_n):
+            raise ValueError("block count does not match geometry")
+        bits = blocks[0].bits
+        for b, nb in zip(blocks, geom.block_n):
+            if b.rows != geom.m or b.cols != nb:
+                raise ValueError(f"block shape {(b.rows, b.cols)} != geometry {(geom.m, nb)}")
+            if b.bits != bits:
+                raise NotImplementedError("mixed bit widths inside one fused linear")
+        db = L.mesw_device_code_bits(bits)
+        if db == 0:
+            raise ValueError(f"bits must be one of (1, 2, 3, 4, 8), got {bits}")
+        dev = torch.device(device)
+        s = _stream(stream)
+        m_pad, n_pad = geom.m_pad, geom.n_pad
+        codes = torch.empty(int(L.mesw_codes_device_bytes(m_pad, n_pad, db)), dtype=torch.uint8, device=dev)
+        steps = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+        for b, cb in zip(blocks, geom.col_base):
+            idx = torch.as_tensor(np.ascontiguousarray(b.salient.indices, dtype=np.int32)).to(dev)
+            packed = torch.frombuffer(bytearray(b.packed.data), dtype=torch.uint8) if b.packed.data else \
+                torch.zeros(1, dtype=torch.uint8)
+            packed = packed.to(dev)
+            _lib.check(L.mesw_repack_codes(packed.data_ptr(), b.rows, b.cols, bits, idx.data_ptr(),
+                                           b.salient.k, codes.data_ptr(), m_pad, n_pad, cb, s))
+            steps[cb:cb + b.cols] = torch.as_tensor(np.ascontiguousarray(b.steps, np.float32)).to(dev)
+        off, sidx, srows = build_salient_tables(blocks, geom)
+        d = cls(geom=geom, bits=bits, code_bits=db, codes=codes, steps=steps,
+                sal_off=off.to(dev), sal_idx=sidx.to(dev), sal_rows=srows.to(dev))
+        d.nbytes = sum(t.numel() * t.element_size() for t in (d.codes, d.steps, d.sal_off, d.sal_idx, d.sal_rows))
+        torch.cuda.current_stream(dev).synchronize() if stream is None else None
+        return d
+
+    def descriptor(self) -> tuple:
+        return (self.codes.data_ptr(), self.steps.data_ptr(), self.sal_off.data_ptr(),
+                self.sal_idx.data_ptr(), self.sal_rows.data_ptr())
+
+    # ---- K6 debug views -------------------------------------------------------
+    def unpack_codes(self, block: int = 0, stream=None) -> torch.Tensor:
+        """int8 [m, n] codes of one block (reference orientation, salient rows read 0)."""
+        L = _lib.lib()
+        g = self.geom
+        out = torch.empty((g.m, g.block_n[block]), dtype=torch.int8, device=self.codes.device)
+        _lib.check(L.mesw_unpack_codes_debug(self.codes.data_ptr(), self.code_bits, g.m, g.block_n[block],
+                                             g.m_pad, g.n_pad, g.col_base[block], out.data_ptr(),
+                                             _stream(stream)))
+        return out
+
+    def reconstruct(self, block: int = 0, stream=None) -> torch.Tensor:
+        """Dense f32 [m, n] = CompressedDelta.reconstruct() (compress.py:115-121), on the GPU."""
+        L = _lib.lib()
+        g = self.geom
+        out = torch.empty((g.m, g.block_n[block]), dtype=torch.float32, device=self.codes.device)
+        _lib.check(L.mesw_dequant_debug(self.codes.data_ptr(), self.code_bits, self.steps.data_ptr(),
+                                        self.sal_off.data_ptr(), self.sal_idx.data_ptr(),
+                                        self.sal_rows.data_ptr(), g.m, g.block_n[block], g.m_pad, g.n_pad,
+                                        g.col_base[block], out.data_ptr(), _stream(stream)))
+        return out
+
+
+def build_salient_tables(blocks: list, geom: LinearGeometry):
+    """Per-column-group salient tables (host C ABI helper) -> (off, idx, rows) CPU tensors."""
+    L = _lib.lib()
+    nb = len(blocks)
+    U32 = C.c_uint32 * nb
+    col_base = U32(*geom.col_base)
+    ns = U32(*[b.cols for b in blocks])
+    ks = U32(*[b.salient.k for b in blocks])
+    idx_arrs = [np.ascontiguousarray(b.salient.indices, dtype=np.uint32) for b in blocks]
+    row_arrs = [np.ascontiguousarray(np.asarray(b.salient_rows, np.float16).view(np.uint16)) for b in blocks]
+    idx_ptrs = (C.c_void_p * nb)(*[a.ctypes.data if a.size else None for a in idx_arrs])
+    row_ptrs = (C.c_void_p * nb)(*[a.ctypes.data if a.size else None for a in row_arrs])
+    total = C.c_uint64()
+    _lib.check(L.mesw_build_salient_tables(nb, col_base, ns, ks, idx_ptrs, row_ptrs, geom.n_pad,
+                                           None, None, None, C.byref(total)))
+    off = np.zeros(geom.n_cg + 1, np.int32)
+    sidx = np.zeros(max(total.value, 1), np.int32)
+    srows = np.zeros((max(total.value, 1), TILE), np.uint16)
+    _lib.check(L.mesw_build_salient_tables(nb, col_base, ns, ks, idx_ptrs, row_ptrs, geom.n_pad,
+                                           off.ctypes.data, sidx.ctypes.data, srows.ctypes.data,
+                                           C.byref(total)))
+    return torch.from_numpy(off), torch.from_numpy(sidx), torch.from_numpy(srows.view(np.int16))
+
+
+# --------------------------------------------------------------------------- base weights
+
+@dataclass
+class DeviceWeight:
+    """Shared base weight (bf16) of one (fused) linear in fragment layout."""
+
+    geom: LinearGeometry
+    frag: torch.Tensor
+
+    @classmethod
+    def empty(cls, geom: LinearGeometry, device="cuda") -> "DeviceWeight":
+        L = _lib.lib()
+        nel = int(L.mesw_weight_device_bytes(geom.m_pad, geom.n_pad)) // 2
+        return cls(geom, torch.zeros(nel, dtype=torch.bfloat16, device=device))
+
+    def load_block(self, block: int, w: torch.Tensor, transposed: bool = False, stream=None) -> None:
+        """Write block `block` from a bf16 device matrix: [m, n] (reference orientation)
+        or [n, m] if `transposed` (torch nn.Linear weight)."""
+        L = _lib.lib()
+        g = self.geom
+        w = w.to(dtype=torch.bfloat16).contiguous()
+        rows, cols = w.shape
+        m, n = (cols, rows) if transposed else (rows, cols)
+        if m != g.m or n != g.block_n[block]:
+            raise ValueError(f"weight shape {tuple(w.shape)} does not match block {block}")
+        _lib.check(L.mesw_repack_weight(w.data_ptr(), m, n, cols, 1 if transposed else 0, self.frag.data_ptr(),
+                                        g.m_pad, g.n_pad, g.col_base[block], _stream(stream)))
+
+    @classmethod
+    def from_dense(cls, blocks: list, device="cuda", transposed: bool = False) -> "DeviceWeight":
+        ts = [torch.as_tensor(b) for b in blocks]
+        m = ts[0].shape[1] if transposed else ts[0].shape[0]
+        ns = tuple(t.shape[0] if transposed else t.shape[1] for t in ts)
+        dw = cls.empty(LinearGeometry(m, ns), device)
+        for i, t in enumerate(ts):
+            dw.load_block(i, t.to(device=device, dtype=torch.bfloat16), transposed)
+        return dw
+
+    def dense(self, block: int = 0, stream=None) -> torch.Tensor:
+        L = _lib.lib()
+        g = self.geom
+        out = torch.empty((g.m, g.block_n[block]), dtype=torch.bfloat16, device=self.frag.device)
+        _lib.check(L.mesw_unpack_weight_debug(self.frag.data_ptr(), g.m, g.block_n[block], g.m_pad, g.n_pad,
+                                              g.col_base[block], out.data_ptr(), _stream(stream)))
+        return out
+
+
+# --------------------------------------------------------------------------- expert table
+
+class ExpertTable:
+    """Device array of mesw_expert_dev descriptors (one slot per resident expert)
+    for one linear.  Slots are stable handles used in segment lists."""
+
+    def __init__(self, device="cuda", capacity: int = 8):
+        self.device = torch.device(device)
+        self.host = np.zeros((capacity, 5), np.int64)
+        self.dev = torch.zeros((capacity, 5), dtype=torch.int64, device=self.device)
+        self.deltas: list = [None] * capacity
+        self.code_bits = None
+
+    def _grow(self, need: int):
+        cap = self.host.shape[0]
+        if need <= cap:
+            return
+        new = max(need, 2 * cap)
+        h = np.zeros((new, 5), np.int64)
+        h[:cap] = self.host
+        self.host = h
+        self.deltas += [None] * (new - cap)
+        self.dev = torch.as_tensor(self.host).to(self.device)
+
+    def set(self, slot: int, delta: DeviceDelta | None) -> None:
+        self._grow(slot + 1)
+        self.deltas[slot] = delta
+        self.host[slot] = delta.descriptor() if delta is not None else 0
+        self.dev[slot] = torch.as_tensor(self.host[slot]).to(self.device)
+        if delta is not None:
+            if self.code_bits not in (None, delta.code_bits):
+                raise NotImplementedError("experts with different device code widths in one table")
+            self.code_bits = delta.code_bits
+
+
+# --------------------------------------------------------------------------- workspace
+
+class Workspace:
+    """Split-K partials + self-resetting column-group counters for one stream."""
+
+    _per_device: dict = {}
+
+    def __init__(self, device):
+        L = _lib.lib()
+        self.device = torch.device(device)
+        idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        with torch.cuda.device(idx):
+            self.sms = L.mesw_device_sm_count()
+        self.nbytes = int(L.mesw_linear_workspace_bytes(64, self.sms))
+        self.ws = torch.empty(self.nbytes, dtype=torch.uint8, device=self.device)
+        self.counters = torch.zeros(1 << 14, dtype=torch.int32, device=self.device)
+
+    @classmethod
+    def get(cls, device) -> "Workspace":
+        device = torch.device(device)
+        key = device.index if device.index is not None else torch.cuda.current_device()
+        if key not in cls._per_device:
+            cls._per_device[key] = cls(torch.device("cuda", key))
+        return cls._per_device[key]
+
+
+# --------------------------------------------------------------------------- K2 call
+
+def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
+              segments, out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
+              out_dtype=torch.bfloat16, geom: LinearGeometry | None = None, num_ctas: int = 0,
+              activation: str | None = None, stream=None) -> torch.Tensor:
+    """y = x.W + x.Dtilde_{expert(t)} (+ residual) in one fused kernel launch.
+
+    x: bf16 [B, ldx] on the GPU with ldx >= m_pad (pad columns zero), rows grouped
+    by expert.  segments: iterable of (begin, end, slot) into `table`.
+    """
+    L = _lib.lib()
+    if geom is None:
+        geom = weight.geom if weight is not None else next(
+            d.geom for d in table.deltas if d is not None)
+    if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_cuda:
+        raise ValueError("x must be a 2-D bf16 CUDA tensor")
+    if x.stride(1) != 1:
+        raise ValueError("x must be row-contiguous")
+    B = x.shape[0]
+    segs = [(int(b), int(e), int(s)) for b, e, s in segments]
+    if out is None:
+        out = torch.empty((B, geom.n), dtype=out_dtype, device=x.device)
+    ws = Workspace.get(x.device)
+    a = _lib.LinearArgs()
+    a.x = x.data_ptr()
+    a.B, a.m, a.n, a.ldx = B, geom.m, geom.n, x.stride(0)
+    a.w = _ptr(weight.frag) if weight is not None else None
+    a.expert_table = table.dev.data_ptr() if table is not None else None
+    a.code_bits = table.code_bits if (table is not None and table.code_bits) else 2
+    a.n_segments = len(segs)
+    if len(segs) > _lib.MAX_SEGMENTS:
+        raise NotImplementedError(f"more than {_lib.MAX_SEGMENTS} expert segments in one launch")
+    for i, (b, e, s) in enumerate(segs):
+        a.seg_begin[i], a.seg_end[i], a.seg_slot[i] = b, e, s
+    a.y = out.data_ptr()
+    a.y_bf16 = 1 if out.dtype == torch.bfloat16 else 0
+    if out.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("output must be bf16 or f32")
+    a.ldy = out.stride(0)
+    if residual is not None:
+        if residual.dtype != torch.bfloat16:
+            raise ValueError("residual must be bf16")
+        a.residual, a.ld_res = residual.data_ptr(), residual.stride(0)
+    a.workspace, a.workspace_bytes = ws.ws.data_ptr(), ws.nbytes
+    a.counters = ws.counters.data_ptr()
+    a.num_ctas = num_ctas
+    a.activation = {None: 0, "relu": 1}[activation]
+    _lib.check(L.mesw_me_linear(C.byref(a), _stream(stream)))
+    return out

@@ -1,0 +1,340 @@
+"""Serving-time API: delta providers, delta_matvec, the batched multi-model forward
+and bench_decode -- the SPEC `infer` module, which the
+reference describes but does not ship, built on the fused GPU kernel.
+
+`GpuCompressedProvider` satisfies the reference's duck-typed provider protocol
+(toylm.py:171-186): `matvec_batch`, `matvec`, `rows`, `row` are METHODS (the
+reference's own CompressedDelta cannot be a provider because its `rows` is an
+int property, compress.py:96-98).  It takes/returns float32 numpy arrays and runs
+every product on the GPU.  Float32 inputs are split into bf16 hi + lo halves
+that the kernel contracts as two token rows, so the delta term is accurate to
+~2^-16 relative (the kernel's own codes, steps and fp16 rows are exact).
+"""
+
+from __future__ import annotations
+
+import statistics
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .compress import CompressedDelta
+from .device import DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, me_linear
+
+__all__ = [
+    "GpuCompressedProvider",
+    "ExactProvider",
+    "LowRankProvider",
+    "ZeroProvider",
+    "delta_matvec",
+    "BatchPlan",
+    "ToyBase",
+    "batched_multi_model_forward",
+    "bench_decode",
+    "split_bf16",
+]
+
+_MAX_ROWS = 32  # hi/lo token pairs per launch (kernel handles <= 64 tokens)
+
+
+def split_bf16(x: torch.Tensor, m_pad: int) -> torch.Tensor:
+    """f32 [T, m] -> bf16 [2T, m_pad]: rows 0..T-1 = bf16(x), rows T.. = bf16(x - hi)."""
+    T, m = x.shape
+    out = torch.zeros((2 * T, m_pad), dtype=torch.bfloat16, device=x.device)
+    hi = x.to(torch.bfloat16)
+    out[:T, :m] = hi
+    out[T:, :m] = (x - hi.to(torch.float32)).to(torch.bfloat16)
+    return out
+
+
+class GpuCompressedProvider:
+    """Compressed delta of one layer, resident on the GPU (SPEC DeltaProvider `Compressed`)."""
+
+    def __init__(self, layer: CompressedDelta, device="cuda"):
+        self.device = torch.device(device)
+        self.delta = DeviceDelta.from_blocks([layer], device=self.device)
+        self.table = ExpertTable(self.device, capacity=1)
+        self.table.set(0, self.delta)
+        self.geom = self.delta.geom
+
+    @property
+    def shape(self) -> tuple:
+        return (self.geom.m, self.geom.n)
+
+    def _run(self, h: torch.Tensor) -> torch.Tensor:
+        T = h.shape[0]
+        outs = []
+        for s in range(0, T, _MAX_ROWS):
+            part = h[s:s + _MAX_ROWS]
+            t = part.shape[0]
+            x2 = split_bf16(part, self.geom.m_pad)
+            y2 = me_linear(x2, None, self.table, [(0, 2 * t, 0)], out_dtype=torch.float32, geom=self.geom)
+            outs.append(y2[:t] + y2[t:])
+        return torch.cat(outs, 0) if outs else torch.zeros((0, self.geom.n), device=self.device)
+
+    def matvec_batch(self, h) -> np.ndarray:
+        """f32 [T, m] -> f32 [T, n] = h . reconstruct() without materialising it."""
+        h = np.asarray(h, dtype=np.float32)
+        if h.ndim != 2 or h.shape[1] != self.geom.m:
+            raise ValueError(f"expected input of shape (T, {self.geom.m}), got {h.shape}")
+        ht = torch.from_numpy(np.ascontiguousarray(h)).to(self.device)
+        return self._run(ht).cpu().numpy()
+
+    def matvec(self, x) -> np.ndarray:
+        x = np.asarray(x, dtype=np.float32)
+        if x.ndim != 1:
+            raise ValueError("matvec expects a 1-D vector")
+        return self.matvec_batch(x[None, :])[0]
+
+    def rows(self, ids) -> np.ndarray:
+        """Delta rows reconstruct()[ids] (embedding layer), bit-exact: one-hot inputs."""
+        ids = np.asarray(ids, dtype=np.int64)
+        if ids.size and (ids.min() < 0 or ids.max() >= self.geom.m):
+            raise ValueError("row id out of range")
+        onehot = torch.zeros((ids.size, self.geom.m), dtype=torch.float32, device=self.device)
+        if ids.size:
+            onehot[torch.arange(ids.size, device=self.device), torch.from_numpy(ids).to(self.device)] = 1.0
+        return self._run(onehot).cpu().numpy()
+
+    def row(self, i) -> np.ndarray:
+        return self.rows(np.asarray([int(i)]))[0]
+
+
+class ExactProvider:
+    """SPEC `Exact(DenseMatrix)`: plain f32 product (library GEMM, not the hot path)."""
+
+    def __init__(self, dense, device="cuda"):
+        self.d = torch.as_tensor(np.asarray(dense, np.float32)).to(device)
+
+    def matvec_batch(self, h):
+        return (torch.as_tensor(np.asarray(h, np.float32)).to(self.d.device) @ self.d).cpu().numpy()
+
+    def matvec(self, x):
+        return self.matvec_batch(np.asarray(x, np.float32)[None])[0]
+
+    def rows(self, ids):
+        return self.d[torch.as_tensor(np.asarray(ids, np.int64)).to(self.d.device)].cpu().numpy()
+
+    def row(self, i):
+        return self.rows([int(i)])[0]
+
+
+class LowRankProvider(ExactProvider):
+    """SPEC `LowRank`: (x.A).B."""
+
+    def __init__(self, a, b, device="cuda"):
+        self.a = torch.as_tensor(np.asarray(a, np.float32)).to(device)
+        self.b = torch.as_tensor(np.asarray(b, np.float32)).to(device)
+        self.d = None
+
+    def matvec_batch(self, h):
+        x = torch.as_tensor(np.asarray(h, np.float32)).to(self.a.device)
+        return ((x @ self.a) @ self.b).cpu().numpy()
+
+    def rows(self, ids):
+        return (self.a[torch.as_tensor(np.asarray(ids, np.int64)).to(self.a.device)] @ self.b).cpu().numpy()
+
+
+class ZeroProvider:
+    """SPEC `Zero`."""
+
+    def __init__(self, shape):
+        self.shape = tuple(shape)
+
+    def matvec_batch(self, h):
+        return np.zeros((np.asarray(h).shape[0], self.shape[1]), np.float32)
+
+    def matvec(self, x):
+        return np.zeros(self.shape[1], np.float32)
+
+    def rows(self, ids):
+        return np.zeros((len(ids), self.shape[1]), np.float32)
+
+    def row(self, i):
+        return np.zeros(self.shape[1], np.float32)
+
+
+def delta_matvec(x, p) -> np.ndarray:
+    """y = x . Dtilde for any provider (Compressed runs the fused GPU kernel)."""
+    x = np.asarray(x, dtype=np.float32)
+    if p is None:
+        raise ValueError("provider is None")
+    return np.asarray(p.matvec(x), np.float32)
+
+
+# --------------------------------------------------------------------------- toy batched forward
+
+@dataclass(frozen=True)
+class BatchPlan:
+    """queries (query id, expert id, token sequence)."""
+
+    queries: tuple
+
+    @classmethod
+    def of(cls, items) -> "BatchPlan":
+        return cls(tuple((q, e, tuple(int(t) for t in toks)) for q, e, toks in items))
+
+
+def _positional_bias(n: int, width: int) -> np.ndarray:
+    """Sinusoidal positional table of the toy model (toylm.py:87-93)."""
+    pos = np.arange(n, dtype=np.float64)[:, None]
+    dim = np.arange(width, dtype=np.float64)[None, :]
+    angle = pos / np.power(10000.0, (2.0 * (dim // 2)) / width)
+    return np.where(dim % 2 == 0, np.sin(angle), np.cos(angle)).astype(np.float32)
+
+
+class ToyBase:
+    """The reference toy model's base weights resident on the GPU (bf16, fragment layout).
+
+    Layer order follows toylm.ToyLM.weight_matrices (embedding, hidden..., head)."""
+
+    def __init__(self, embedding, layers, head, device="cuda"):
+        self.device = torch.device(device)
+        self.embedding = torch.as_tensor(np.asarray(embedding, np.float32)).to(self.device)
+        self.vocab, self.width = self.embedding.shape
+        self.layers = [DeviceWeight.from_dense([np.asarray(w, np.float32)], self.device) for w in layers]
+        self.head = DeviceWeight.from_dense([np.asarray(head, np.float32)], self.device)
+        self.depth = len(self.layers)
+
+    @classmethod
+    def from_model(cls, model, device="cuda") -> "ToyBase":
+        return cls(model.embedding, model.layers, model.head, device)
+
+    @property
+    def n_weight_layers(self) -> int:
+        return self.depth + 2
+
+
+class ExpertSet:
+    """Resident experts of a toy model: one ExpertTable per weight layer."""
+
+    def __init__(self, base: ToyBase):
+        self.base = base
+        self.tables = [ExpertTable(base.device) for _ in range(base.n_weight_layers)]
+        self.slots: dict = {}
+
+    def add(self, expert_id, artifact) -> int:
+        layers = artifact.layers if hasattr(artifact, "layers") else list(artifact)
+        if len(layers) != self.base.n_weight_layers:
+            raise ValueError("artifact layer count does not match the base model")
+        slot = len(self.slots)
+        for t, layer in zip(self.tables, layers):
+            t.set(slot, DeviceDelta.from_blocks([layer], device=self.base.device))
+        self.slots[expert_id] = slot
+        return slot
+
+
+def batched_multi_model_forward(base: ToyBase, experts: ExpertSet, plan) -> list:
+    """SPEC.md:433-438 on the GPU: shared-base x.W and every expert group's delta in
+    ONE fused launch per layer; per-query results in input order.
+
+    Returns [(query_id, logits f32 [len, V] or None, error or None)].  An unknown
+    expert yields an error entry for that query and the batch continues.
+    Numerics: bf16 activations/base weights, f32 accumulation (tolerance: DESIGN.md).
+    """
+    queries = plan.queries if isinstance(plan, BatchPlan) else tuple(plan)
+    results = {}
+    order = []
+    for qi, (qid, eid, toks) in enumerate(queries):
+        if eid not in experts.slots:
+            results[qi] = (qid, None, f"unknown expert {eid!r}")
+        elif len(toks) == 0:
+            results[qi] = (qid, None, "empty token sequence")
+        else:
+            order.append(qi)
+    # group the valid queries by expert slot (stable), concatenate their positions
+    order.sort(key=lambda qi: experts.slots[queries[qi][1]])
+    dev = base.device
+    ids, pos, spans, segs = [], [], {}, []
+    cur = 0
+    for qi in order:
+        toks = np.asarray(queries[qi][2], np.int64)
+        if toks.min() < 0 or toks.max() >= base.vocab:
+            results[qi] = (queries[qi][0], None, "token id out of range")
+            continue
+        slot = experts.slots[queries[qi][1]]
+        spans[qi] = (cur, cur + toks.size)
+        if segs and segs[-1][2] == slot and segs[-1][1] == cur:
+            segs[-1] = (segs[-1][0], cur + toks.size, slot)
+        else:
+            segs.append((cur, cur + toks.size, slot))
+        ids.append(toks)
+        pos.append(np.arange(toks.size))
+        cur += toks.size
+    if cur:
+        all_ids = torch.from_numpy(np.concatenate(ids)).to(dev)
+        pb = torch.from_numpy(_positional_bias(max(int(p.max()) for p in pos) + 1, base.width)).to(dev)
+        h = base.embedding[all_ids] + pb[torch.from_numpy(np.concatenate(pos)).to(dev)]
+        # embedding delta: one-hot rows through the fused kernel (exact rows of reconstruct())
+        logits = torch.empty((cur, base.vocab), dtype=torch.float32, device=dev)
+        hs = []
+        for c0 in range(0, cur, 64):
+            c1 = min(cur, c0 + 64)
+            csegs = _clip_segments(segs, c0, c1)
+            onehot = torch.zeros((c1 - c0, _pad128(base.vocab)), dtype=torch.bfloat16, device=dev)
+            onehot[torch.arange(c1 - c0, device=dev), all_ids[c0:c1]] = 1.0
+            emb_delta = me_linear(onehot, None, experts.tables[0], csegs, out_dtype=torch.float32,
+                                  geom=LinearGeometry(base.vocab, (base.width,)))
+            x = h[c0:c1] + emb_delta
+            for li, w in enumerate(base.layers):
+                xb = _pad_cols(x.to(torch.bfloat16), w.geom.m_pad)
+                x = me_linear(xb, w, experts.tables[1 + li], csegs, out_dtype=torch.float32, activation="relu")
+            xb = _pad_cols(x.to(torch.bfloat16), base.head.geom.m_pad)
+            me_linear(xb, base.head, experts.tables[-1], csegs, out=logits[c0:c1])
+        out_np = logits.cpu().numpy()
+        for qi, (a, b) in spans.items():
+            results[qi] = (queries[qi][0], out_np[a:b].copy(), None)
+    return [results[i] for i in range(len(queries))]
+
+
+def _pad128(v: int) -> int:
+    return (v + 127) // 128 * 128
+
+
+def _pad_cols(x: torch.Tensor, width: int) -> torch.Tensor:
+    if x.shape[1] == width:
+        return x.contiguous()
+    out = torch.zeros((x.shape[0], width), dtype=x.dtype, device=x.device)
+    out[:, :x.shape[1]] = x
+    return out
+
+
+def _clip_segments(segs, c0: int, c1: int) -> list:
+    out = []
+    for b, e, s in segs:
+        b2, e2 = max(b, c0), min(e, c1)
+        if b2 < e2:
+            out.append((b2 - c0, e2 - c0, s))
+    return out
+
+
+# --------------------------------------------------------------------------- bench_decode
+
+def bench_decode(weight: DeviceWeight, table: ExpertTable, segments, x: torch.Tensor,
+                 repetitions: int = 20, warmup: int = 3) -> dict:
+    """SPEC.md:439-443 (Appendix F decomposition) for one multi-expert linear:
+    base GEMV alone, delta stage alone, and the fused kernel; CUDA-event timed,
+    first `warmup` reps dropped, median and p90 in milliseconds."""
+
+    def timeit(fn):
+        samples = []
+        for r in range(repetitions + warmup):
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            st.record()
+            fn()
+            en.record()
+            en.synchronize()
+            if r >= warmup:
+                samples.append(st.elapsed_time(en))
+        samples.sort()
+        p90 = samples[min(len(samples) - 1, int(round(0.9 * (len(samples) - 1))))]
+        return {"median": statistics.median(samples), "p90": p90, "n": len(samples),
+                "flag": "no-variance" if len(samples) == 1 else None}
+
+    geom = weight.geom
+    base = timeit(lambda: me_linear(x, weight, None, [], geom=geom))
+    delta = timeit(lambda: me_linear(x, None, table, segments, geom=geom)) if segments else \
+        {"median": 0.0, "p90": 0.0, "n": 0, "flag": None}
+    total = timeit(lambda: me_linear(x, weight, table, segments, geom=geom))
+    return {"base_gemm_ms": base, "delta_stage_ms": delta, "total_ms": total}

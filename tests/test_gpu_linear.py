@@ -1,0 +1,219 @@
+"""GPU parity of the loader (K1), debug decoders (K6) and the fused multi-expert
+linear (K2) against the oracle and the reference golden fixtures."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import mesw as om
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _read(name):
+    with open(os.path.join(GOLDEN, name), "rb") as f:
+        return f.read()
+
+
+def _layer_names():
+    with open(os.path.join(GOLDEN, "kat.json")) as f:
+        return json.load(f)["layers"]
+
+
+def _art_layer(olayer):
+    from paper_2406_09041_b200 import compress
+    man = {"model_id": "t", "domain": "d", "base_digest": "0", "layer_count": 1}
+    return compress.deserialize_artifact(om.serialize_artifact(man, [olayer])).layers[0]
+
+
+def test_repack_and_unpack_bit_exact_on_reference_layers():
+    from paper_2406_09041_b200 import compress
+    from paper_2406_09041_b200.device import DeviceDelta
+    z = np.load(os.path.join(GOLDEN, "layer_expected.npz"))
+    for name in _layer_names():
+        L = compress.load_artifact(os.path.join(GOLDEN, f"layer_{name}.mesw")).layers[0]
+        d = DeviceDelta.from_blocks([L])
+        codes = d.unpack_codes().cpu().numpy()
+        ref = z[f"{name}_codes"].copy()
+        ref[z[f"{name}_salient"]] = 0  # the reference writes salient codes as 0 (compress.py:205-214)
+        assert np.array_equal(codes, ref), name
+        # K6 dense reconstruction == reference reconstruct(), bit for bit
+        rec = d.reconstruct().cpu().numpy()
+        assert np.array_equal(rec, z[f"{name}_recon"]), name
+
+
+@pytest.mark.parametrize("bits", [1, 2, 3, 4, 8])
+def test_repack_random_codes_all_widths(bits):
+    from paper_2406_09041_b200.device import DeviceDelta
+    rng = np.random.default_rng(bits)
+    for (m, n, k) in [(1, 1, 0), (129, 257, 3), (384, 130, 0), (256, 512, 8)]:
+        k = 0 if bits == 1 else min(k, m)
+        ol = om.random_layer(rng, m, n, bits, k)
+        d = DeviceDelta.from_blocks([_art_layer(ol)])
+        ref = ol.codes().copy()
+        ref[ol.salient_idx] = 0
+        assert np.array_equal(d.unpack_codes().cpu().numpy(), ref)
+        assert np.array_equal(d.reconstruct().cpu().numpy(), ol.reconstruct())
+
+
+def test_weight_repack_roundtrip():
+    torch = _torch()
+    from paper_2406_09041_b200.device import DeviceWeight
+    g = torch.Generator().manual_seed(0)
+    w = torch.randn(300, 200, generator=g).to(torch.bfloat16).cuda()
+    dw = DeviceWeight.from_dense([w])
+    assert torch.equal(dw.dense(), w)
+    wt = torch.randn(130, 257, generator=g).to(torch.bfloat16).cuda()  # nn.Linear [out, in]
+    dw2 = DeviceWeight.from_dense([wt], transposed=True)
+    assert torch.equal(dw2.dense(), wt.t())
+
+
+def test_provider_matches_reference_layers():
+    """Delta-only fused kernel (hi/lo f32 split) vs reference x @ reconstruct() (1e-5)."""
+    from paper_2406_09041_b200 import compress
+    from paper_2406_09041_b200.infer import GpuCompressedProvider
+    z = np.load(os.path.join(GOLDEN, "layer_expected.npz"))
+    for name in _layer_names():
+        L = compress.load_artifact(os.path.join(GOLDEN, f"layer_{name}.mesw")).layers[0]
+        p = GpuCompressedProvider(L)
+        y = p.matvec_batch(z[f"{name}_x"])
+        ref = z[f"{name}_y"]
+        err = np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30)
+        assert err <= 1e-5, (name, err)
+        # rows(ids) is bit-exact with reconstruct()[ids]
+        ids = np.array([0, 3, L.rows - 1])
+        assert np.array_equal(p.rows(ids), z[f"{name}_recon"][ids])
+        assert np.allclose(p.matvec(z[f"{name}_x"][0]), ref[0], rtol=1e-5, atol=1e-5 * np.abs(ref).max())
+
+
+def _setup_linear(m, ns, n_experts, bits=2, k=8, seed=0, device="cuda"):
+    torch = _torch()
+    from paper_2406_09041_b200.device import DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry
+    rng = np.random.default_rng(seed)
+    geom = LinearGeometry(m, tuple(ns))
+    w_blocks = [rng.normal(0, 0.02, size=(m, n)).astype(np.float32) for n in ns]
+    dw = DeviceWeight.empty(geom, device)
+    for b, wb in enumerate(w_blocks):
+        dw.load_block(b, torch.from_numpy(wb).to(device).to(torch.bfloat16))
+    w_bf = [torch.from_numpy(wb).to(torch.bfloat16).to(torch.float32).numpy() for wb in w_blocks]
+    table = ExpertTable(device)
+    experts = []
+    for e in range(n_experts):
+        blocks = [om.random_layer(rng, m, n, bits, min(k, m) if bits != 1 else 0) for n in ns]
+        experts.append(blocks)
+        table.set(e, DeviceDelta.from_blocks([_art_layer(b) for b in blocks], geom, device))
+    return geom, dw, w_bf, table, experts
+
+
+def _oracle_linear(x_bf, w_bf, experts, segs, geom, B):
+    """f64 oracle on the same bf16-rounded inputs: x.W + x.reconstruct_e."""
+    n = geom.n
+    y = np.zeros((B, n), np.float64)
+    for b, cb in enumerate(geom.col_base):
+        nb = geom.block_n[b]
+        y[:, cb:cb + nb] = x_bf.astype(np.float64) @ w_bf[b].astype(np.float64)
+    for (s0, s1, slot) in segs:
+        for b, cb in enumerate(geom.col_base):
+            nb = geom.block_n[b]
+            y[s0:s1, cb:cb + nb] += om.delta_matvec_batch(x_bf[s0:s1], experts[slot][b])
+    return y
+
+
+def _rel(y, ref):
+    return float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+@pytest.mark.parametrize("B,segs,num_ctas", [
+    (1, [(0, 1, 0)], 0),
+    (5, [(0, 2, 1), (2, 5, 0)], 0),
+    (8, [(0, 3, 0), (3, 6, 1), (6, 8, 2)], 0),
+    (8, [(0, 3, 0), (3, 6, 1), (6, 8, 2)], 7),
+    (13, [(0, 4, 2), (6, 13, 1)], 13),
+    (32, [(0, 11, 0), (11, 22, 1), (22, 32, 2)], 0),
+    (64, [(i * 4, i * 4 + 4, i % 3) for i in range(16)], 0),
+    (20, [], 0),
+])
+def test_fused_linear_matches_oracle(B, segs, num_ctas):
+    torch = _torch()
+    from paper_2406_09041_b200.device import me_linear
+    geom, dw, w_bf, table, experts = _setup_linear(384, (256, 128), 3, seed=B)
+    rng = np.random.default_rng(100 + B)
+    x = torch.from_numpy(rng.normal(0, 1, size=(B, geom.m_pad)).astype(np.float32)).to(torch.bfloat16).cuda()
+    y = me_linear(x, dw, table, segs, out_dtype=torch.float32, num_ctas=num_ctas).cpu().numpy()
+    ref = _oracle_linear(x.float().cpu().numpy()[:, :geom.m], w_bf, experts, segs, geom, B)
+    assert _rel(y, ref) <= 2e-3
+    # bf16 output + residual epilogue
+    res = torch.from_numpy(rng.normal(0, 1, size=(B, geom.n)).astype(np.float32)).to(torch.bfloat16).cuda()
+    y2 = me_linear(x, dw, table, segs, residual=res, num_ctas=num_ctas).float().cpu().numpy()
+    assert _rel(y2, ref + res.float().cpu().numpy()) <= 1e-2
+
+
+@pytest.mark.parametrize("bits", [1, 3, 4, 8])
+def test_fused_linear_other_widths(bits):
+    torch = _torch()
+    from paper_2406_09041_b200.device import me_linear
+    geom, dw, w_bf, table, experts = _setup_linear(256, (384,), 2, bits=bits, k=4, seed=bits)
+    rng = np.random.default_rng(bits)
+    B, segs = 9, [(0, 4, 1), (4, 9, 0)]
+    x = torch.from_numpy(rng.normal(0, 1, size=(B, geom.m_pad)).astype(np.float32)).to(torch.bfloat16).cuda()
+    y = me_linear(x, dw, table, segs, out_dtype=torch.float32).cpu().numpy()
+    ref = _oracle_linear(x.float().cpu().numpy()[:, :geom.m], w_bf, experts, segs, geom, B)
+    assert _rel(y, ref) <= 2e-3
+
+
+def test_batch_composition_invariance_bitwise():
+    """a query's result does not depend on the rest of the batch (exact)."""
+    torch = _torch()
+    from paper_2406_09041_b200.device import me_linear
+    geom, dw, w_bf, table, experts = _setup_linear(512, (384,), 3, seed=11)
+    rng = np.random.default_rng(5)
+    X = torch.from_numpy(rng.normal(0, 1, size=(24, geom.m_pad)).astype(np.float32)).to(torch.bfloat16).cuda()
+    expert_of = rng.integers(0, 3, size=24)
+    order = np.argsort(expert_of, kind="stable")
+    segs, cur = [], 0
+    for e in range(3):
+        cnt = int((expert_of == e).sum())
+        if cnt:
+            segs.append((cur, cur + cnt, e))
+        cur += cnt
+    y_full = me_linear(X[torch.from_numpy(order).cuda()].contiguous(), dw, table, segs,
+                       out_dtype=torch.float32).cpu().numpy()
+    for pos, q in enumerate(order):
+        e = int(expert_of[q])
+        y1 = me_linear(X[q:q + 1].contiguous(), dw, table, [(0, 1, e)], out_dtype=torch.float32).cpu().numpy()
+        assert np.array_equal(y1[0], y_full[pos])
+    # different expert order in the batch -> same bits per query
+    perm = [2, 0, 1]
+    order2 = np.concatenate([np.flatnonzero(expert_of == e) for e in perm])
+    segs2, cur = [], 0
+    for e in perm:
+        cnt = int((expert_of == e).sum())
+        segs2.append((cur, cur + cnt, e))
+        cur += cnt
+    y_perm = me_linear(X[torch.from_numpy(order2).cuda()].contiguous(), dw, table, segs2,
+                       out_dtype=torch.float32).cpu().numpy()
+    pos_full = {int(q): i for i, q in enumerate(order)}
+    for i, q in enumerate(order2):
+        assert np.array_equal(y_perm[i], y_full[pos_full[int(q)]])
+
+
+def test_c1_shape_mixed_decode():
+    """BASELINE config 1 shape: 4096x14336, 3 experts (2-bit, k=8), batch-8 mixed decode."""
+    torch = _torch()
+    from paper_2406_09041_b200.device import me_linear
+    geom, dw, w_bf, table, experts = _setup_linear(4096, (14336,), 3, seed=1)
+    rng = np.random.default_rng(7)
+    x = torch.from_numpy(rng.normal(0, 1, size=(8, 4096)).astype(np.float32)).to(torch.bfloat16).cuda()
+    # experts t mod 3 -> grouped order
+    segs = [(0, 3, 0), (3, 6, 1), (6, 8, 2)]
+    y = me_linear(x, dw, table, segs, out_dtype=torch.float32).cpu().numpy()
+    ref = _oracle_linear(x.float().cpu().numpy(), w_bf, experts, segs, geom, 8)
+    assert _rel(y, ref) <= 2e-3
