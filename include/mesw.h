@@ -175,6 +175,36 @@ typedef struct {
 uint64_t mesw_linear_workspace_bytes(int32_t B, int32_t num_ctas);
 int mesw_me_linear(const mesw_linear_args* args, void* stream);
 
+/* ------------------------------------- K5: Mistral decoder glue (decode step)
+ * The reference toy model has no attention (toylm.py:1-8); these are the
+ * standard decoder pieces around the fused linears of the Mistral-shaped
+ * serving stack.  bf16 storage, f32 arithmetic.              */
+/* out[b, :] = table[ids[b], :]  (embedding gather; toylm.py:165 `embedding[ids]`) */
+int mesw_embed(const int32_t* d_ids, int B, const uint16_t* d_table, int H, uint16_t* d_out,
+               int ld_out, void* stream);
+/* y = x * rsqrt(mean(x^2) + eps) * w */
+int mesw_rmsnorm(const uint16_t* d_x, int ldx, const uint16_t* d_w, int B, int H, float eps,
+                 uint16_t* d_y, int ldy, void* stream);
+/* RoPE (rotate-half) on the q and k heads of a fused qkv row, append k/v to the
+ * caches [B][ctx_max][n_kv][head_dim] at position pos[b]. */
+int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_pos, int B, int n_heads,
+                     int n_kv, int head_dim, float theta, uint16_t* d_kcache,
+                     uint16_t* d_vcache, int ctx_max, void* stream);
+/* GQA decode attention over len[b] cached positions; out [B][n_heads*head_dim]. */
+int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
+                          const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
+                          int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
+                          void* stream);
+/* out = silu(gate) * up for rows [gate(I) | up(I)]. */
+int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,
+                void* stream);
+/* Greedy next token: argmax with ties to the lowest id (toylm.py:247). */
+int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int ld, int32_t* d_out,
+                void* stream);
+/* Decode bookkeeping: pos[b] += 1 (wrapping to wrap_to at ctx_max), len[b] = pos[b] + 1. */
+int mesw_advance_positions(int32_t* d_pos, int32_t* d_len, int B, int ctx_max, int wrap_to,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

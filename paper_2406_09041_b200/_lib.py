@@ -67,6 +67,16 @@ _SIGNATURES = [
                                            C.c_uint32, C.c_void_p, C.c_void_p]),
     ("mesw_linear_workspace_bytes", C.c_uint64, [C.c_int32, C.c_int32]),
     ("mesw_me_linear", C.c_int, [C.POINTER(LinearArgs), C.c_void_p]),
+    ("mesw_embed", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
+    ("mesw_rmsnorm", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p,
+                               C.c_int, C.c_void_p]),
+    ("mesw_rope_append", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_float, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    ("mesw_attention_decode", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
+    ("mesw_swiglu", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
+    ("mesw_argmax", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    ("mesw_advance_positions", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
 ]
 
 SYMBOLS = [s[0] for s in _SIGNATURES]

@@ -25,8 +25,6 @@
 
 namespace mesw {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kXStride = kTileK + 8;  // bf16 elements per x row in smem (272 B, conflict-free)
 constexpr int kMaxSegsPerStage = 16;
 
@@ -146,58 +144,86 @@ __device__ __forceinline__ void epilogue(const LinearParams& p, const SegDesc* s
 }
 
 // ---------------------------------------------------------------- kernel
+// NT: n-tiles of 8 tokens.  KSPLIT: consumer warps per 16-output tile (each takes
+// 8/KSPLIT of the unit's 8 k-blocks); NACC: independent accumulator sets (k-block
+// parity) to break the mma dependency chain when there is a single n-tile.
+template <int NT>
+struct Cfg {
+  static constexpr int KSPLIT = NT <= 2 ? 2 : 1;
+  static constexpr int NACC = NT == 1 ? 2 : 1;
+  static constexpr int CW = kTilesPerCg * KSPLIT;  // consumer warps
+  static constexpr int THREADS = (CW + 1) * 32;
+  static constexpr int KB2 = kKbPerKs / 2 / KSPLIT;  // k-block pairs per warp per unit
+  static constexpr int XCHG = KSPLIT == 2 ? kTilesPerCg * NT * 32 * 8 * 4 : 0;
+};
+
+__host__ __device__ inline size_t header_bytes(int S, int NT, int xchg) {
+  const size_t raw = (size_t)S * 16 + 16 + (size_t)NT * 8 * 4 + MESW_MAX_SEGMENTS * sizeof(SegDesc);
+  return ((raw + 15) & ~size_t(15)) + xchg + 1023 & ~size_t(1023);
+}
+
+template <int NT>
+__device__ __forceinline__ void load_x_frags(uint32_t (&b)[NT][4], const uint16_t* xl, int kb2) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+    ldmatrix_x4(b[nt][0], b[nt][1], b[nt][2], b[nt][3], xl + nt * 8 * kXStride + kb2 * 32);
+}
+
 template <int DB, int NT>
-__global__ void __launch_bounds__(kThreads, 1) me_linear_kernel(const __grid_constant__ LinearParams p) {
+__global__ void __launch_bounds__(Cfg<NT>::THREADS, 1)
+    me_linear_kernel(const __grid_constant__ LinearParams p) {
+  using C = Cfg<NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int S = p.n_stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + S;
   int* flag = reinterpret_cast<int*>(empty + S);
-  int* tok2seg = flag + 4;                                 // [NT*8]
+  int* tok2seg = flag + 4;                                       // [NT*8]
   SegDesc* segs = reinterpret_cast<SegDesc*>(tok2seg + NT * 8);  // [n_seg]
-  const size_t hdr = (((size_t)(S * 16 + 16 + NT * 8 * 4 + MESW_MAX_SEGMENTS * sizeof(SegDesc))) + 1023) & ~size_t(1023);
-  uint8_t* ring = smem + hdr;
+  const size_t raw = (size_t)S * 16 + 16 + (size_t)NT * 8 * 4 + MESW_MAX_SEGMENTS * sizeof(SegDesc);
+  float* xchg = reinterpret_cast<float*>(smem + ((raw + 15) & ~size_t(15)));
+  uint8_t* ring = smem + header_bytes(S, NT, C::XCHG);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const long long u0 = (long long)c * p.T / p.G, u1 = (long long)(c + 1) * p.T / p.G;
   constexpr int CB = kTileN * kTileK * DB / 8;  // code bytes per (cg, ks)
   constexpr int CBL = 8 * DB;                   // code bytes per lane per ks
+  constexpr int CBW = CBL / C::KSPLIT;          // ... per warp-lane share
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], C::CW);
     }
     fence_mbar_init();
   }
-  for (int i = threadIdx.x; i < NT * 8; i += kThreads) tok2seg[i] = -1;
+  for (int i = threadIdx.x; i < NT * 8; i += C::THREADS) tok2seg[i] = -1;
   __syncthreads();
-  for (int s = threadIdx.x; s < p.n_seg; s += kThreads) {
-    const mesw_expert_dev e = p.table[p.seg_slot[s]];
+  for (int q = threadIdx.x; q < p.n_seg; q += C::THREADS) {
+    const mesw_expert_dev e = p.table[p.seg_slot[q]];
     SegDesc d;
     d.codes = reinterpret_cast<const uint8_t*>(e.codes);
     d.steps = e.steps;
     d.sal_off = e.sal_off;
     d.sal_idx = e.sal_idx;
     d.sal_rows = e.sal_rows;
-    d.begin = p.seg_begin[s];
-    d.end = p.seg_end[s];
-    segs[s] = d;
-    for (int t = d.begin; t < d.end; ++t) tok2seg[t] = s;
+    d.begin = p.seg_begin[q];
+    d.end = p.seg_end[q];
+    segs[q] = d;
+    for (int t = d.begin; t < d.end; ++t) tok2seg[t] = q;
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
+  if (warp == C::CW) {
     // ===================== producer warp =====================
-    long long it = 0;
+    int s = 0;
+    uint32_t ph = 0;
+    bool first_pass = true;
+    int ks = (int)(u0 % p.n_ks);
     for (long long u = u0; u < u1; ++u) {
-      const long long unit = u;  // == cg * n_ks + ks
-      const int ks = (int)(u % p.n_ks);
-      for (int ch = 0; ch < p.n_chunks; ++ch, ++it) {
-        const int s = (int)(it % S);
-        const uint32_t use = (uint32_t)(it / S);
-        if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      for (int ch = 0; ch < p.n_chunks; ++ch) {
+        if (!first_pass) mbar_wait(&empty[s], ph ^ 1);
         const bool do_w = (p.w != nullptr) && ch == 0;
         const int sg0 = ch * p.segs_per_stage;
         const int sg1 = min(p.n_seg, sg0 + p.segs_per_stage);
@@ -207,56 +233,72 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_kernel(const __grid_con
         if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
         __syncwarp();
         if (do_w && lane == 0)
-          bulk_g2s(st, p.w + (size_t)unit * kWBytesPerUnit, kWBytesPerUnit, &full[s]);
+          bulk_g2s(st, p.w + (size_t)u * kWBytesPerUnit, kWBytesPerUnit, &full[s]);
         for (int q = sg0 + lane; q < sg1; q += 32)
-          bulk_g2s(st + p.codes_off + (size_t)(q - sg0) * CB, segs[q].codes + (size_t)unit * CB, CB,
+          bulk_g2s(st + p.codes_off + (size_t)(q - sg0) * CB, segs[q].codes + (size_t)u * CB, CB,
                    &full[s]);
         for (int r = lane; r < p.B; r += 32)
           bulk_g2s(st + p.x_off + (size_t)r * kXStride * 2,
                    p.x + (size_t)r * p.ldx + (size_t)ks * kTileK, kTileK * 2, &full[s]);
         __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; first_pass = false; }
       }
+      if (++ks == p.n_ks) ks = 0;
     }
     return;
   }
 
   // ===================== consumer warps =====================
-  float accB[NT][4], accD[NT][4];
+  const int tile = warp & (kTilesPerCg - 1);
+  const int kh = warp / kTilesPerCg;  // k-split index
+  float accB[C::NACC][NT][4], accD[C::NACC][NT][4];
   const int cg_first = (int)(u0 / p.n_ks);
-  long long it = 0;
+  int cg = cg_first, ks = (int)(u0 % p.n_ks);
+  int s = 0;
+  uint32_t ph = 0;
   long long piece_start = u0;
   for (long long u = u0; u < u1; ++u) {
-    const int cg = (int)(u / p.n_ks), ks = (int)(u % p.n_ks);
     if (u == u0 || ks == 0) {
       piece_start = u;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int a = 0; a < C::NACC; ++a)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) accB[nt][i] = accD[nt][i] = 0.f;
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) accB[a][nt][i] = accD[a][nt][i] = 0.f;
     }
-    for (int ch = 0; ch < p.n_chunks; ++ch, ++it) {
-      const int s = (int)(it % S);
-      mbar_wait(&full[s], (uint32_t)((it / S) & 1));
+    for (int ch = 0; ch < p.n_chunks; ++ch) {
+      mbar_wait(&full[s], ph);
       const uint8_t* st = ring + (size_t)s * p.stage_bytes;
       const uint16_t* xs = reinterpret_cast<const uint16_t*>(st + p.x_off);
       // ldmatrix row address for this lane: token row (lane&7), k offset (lane>>3)*8
       const uint16_t* xl = xs + (lane & 7) * kXStride + (lane >> 3) * 8;
+      const int kb2_0 = kh * C::KB2;
+
+      // x fragments of this warp's k-blocks (hoisted when they fit in registers)
+      uint32_t bx[C::KSPLIT == 2 ? C::KB2 : 1][NT][4];
+      if constexpr (C::KSPLIT == 2) {
+#pragma unroll
+        for (int j = 0; j < C::KB2; ++j) load_x_frags<NT>(bx[j], xl, kb2_0 + j);
+      }
 
       if (p.w != nullptr && ch == 0) {
-        const uint4* Ws = reinterpret_cast<const uint4*>(st) + (warp * kKbPerKs) * 32 + lane;
+        const uint4* Ws = reinterpret_cast<const uint4*>(st) + (tile * kKbPerKs) * 32 + lane;
 #pragma unroll
-        for (int kb2 = 0; kb2 < kKbPerKs / 2; ++kb2) {
-          uint32_t b[NT][4];
+        for (int j = 0; j < C::KB2; ++j) {
+          uint32_t bl[NT][4];
+          if constexpr (C::KSPLIT != 2) load_x_frags<NT>(bl, xl, kb2_0 + j);
+          const uint4 w0 = Ws[(2 * (kb2_0 + j)) * 32];
+          const uint4 w1 = Ws[(2 * (kb2_0 + j) + 1) * 32];
+          const uint32_t a0[4] = {w0.x, w0.y, w0.z, w0.w};
+          const uint32_t a1[4] = {w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-            ldmatrix_x4(b[nt][0], b[nt][1], b[nt][2], b[nt][3], xl + nt * 8 * kXStride + kb2 * 32);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint4 wv = Ws[(2 * kb2 + h) * 32];
-            const uint32_t a[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-              if (nt * 8 < p.B) mma_bf16(accB[nt], a, b[nt][2 * h], b[nt][2 * h + 1]);
+          for (int nt = 0; nt < NT; ++nt) {
+            if (nt * 8 < p.B) {
+              const uint32_t* bb = C::KSPLIT == 2 ? bx[C::KSPLIT == 2 ? j : 0][nt] : bl[nt];
+              mma_bf16(accB[0][nt], a0, bb[0], bb[1]);
+              mma_bf16(accB[C::NACC - 1][nt], a1, bb[2], bb[3]);
+            }
           }
         }
       }
@@ -266,86 +308,142 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_kernel(const __grid_con
       for (int q = sg0; q < sg1; ++q) {
         const int sb = segs[q].begin, se = segs[q].end;
         const int lo_nt = sb >> 3, hi_nt = (se - 1) >> 3;
-        uint32_t cw[CBL / 4];
-        const uint8_t* cl = st + p.codes_off + (size_t)(q - sg0) * CB + (size_t)(warp * 32 + lane) * CBL;
+        uint32_t cw[CBL / 4];  // full-unit word array; this warp reads its share only
+        const uint8_t* cl = st + p.codes_off + (size_t)(q - sg0) * CB +
+                            (size_t)(tile * 32 + lane) * CBL + kh * CBW;
+        if constexpr (CBW == 8) {
+          const uint2 t2 = *reinterpret_cast<const uint2*>(cl);
+          cw[kh * 2 + 0] = t2.x; cw[kh * 2 + 1] = t2.y;
+        } else {
 #pragma unroll
-        for (int v = 0; v < CBL / 16; ++v) {
-          const uint4 t4 = lds128(cl + v * 16);
-          cw[4 * v + 0] = t4.x; cw[4 * v + 1] = t4.y; cw[4 * v + 2] = t4.z; cw[4 * v + 3] = t4.w;
+          for (int v = 0; v < CBW / 16; ++v) {
+            const uint4 t4 = lds128(cl + v * 16);
+            const int w0 = kh * (CBW / 4) + 4 * v;
+            cw[w0 + 0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
+          }
+        }
+        // lane's B-fragment token for each n-tile, and whether it belongs to this segment
+        bool mine[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int tok = nt * 8 + (lane >> 2);
+          mine[nt] = tok >= sb && tok < se;
         }
 #pragma unroll
-        for (int kb2 = 0; kb2 < kKbPerKs / 2; ++kb2) {
-          uint32_t b[NT][4];
+        for (int j = 0; j < C::KB2; ++j) {
+          uint32_t bm[NT][4];
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             if (nt >= lo_nt && nt <= hi_nt) {
-              ldmatrix_x4(b[nt][0], b[nt][1], b[nt][2], b[nt][3], xl + nt * 8 * kXStride + kb2 * 32);
-              const int tok = nt * 8 + (lane >> 2);  // B-fragment column owned by this lane
-              if (tok < sb || tok >= se) b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = 0u;
+              if constexpr (C::KSPLIT == 2) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) bm[nt][r] = mine[nt] ? bx[C::KSPLIT == 2 ? j : 0][nt][r] : 0u;
+              } else {
+                ldmatrix_x4(bm[nt][0], bm[nt][1], bm[nt][2], bm[nt][3],
+                            xl + nt * 8 * kXStride + (kb2_0 + j) * 32);
+                if (!mine[nt]) bm[nt][0] = bm[nt][1] = bm[nt][2] = bm[nt][3] = 0u;
+              }
             }
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint32_t a[4];
-            dequant_kb<DB>(cw, 2 * kb2 + h, a);
+            dequant_kb<DB>(cw, 2 * (kb2_0 + j) + h, a);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
-              if (nt >= lo_nt && nt <= hi_nt) mma_bf16(accD[nt], a, b[nt][2 * h], b[nt][2 * h + 1]);
+              if (nt >= lo_nt && nt <= hi_nt)
+                mma_bf16(accD[h % C::NACC][nt], a, bm[nt][2 * h], bm[nt][2 * h + 1]);
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) { s = 0; ph ^= 1; }
     }
 
     // ---- end of a piece: full column group, or a range boundary ----
     if (ks == p.n_ks - 1 || u == u1 - 1) {
-      const bool whole = (piece_start == (long long)cg * p.n_ks) && (ks == p.n_ks - 1);
-      if (whole) {
-        epilogue<NT>(p, segs, tok2seg, cg, warp, lane, accB, accD);
-      } else {
-        const int slot = 2 * c + (cg == cg_first ? 0 : 1);
-        const size_t slot_floats = (size_t)kConsumerWarps * NT * 32 * 8;
-        float* mine = p.ws + (size_t)slot * slot_floats + ((size_t)warp * NT * 32 + lane) * 8;
+      // fold accumulator sets (fixed order), then the k-split halves through smem
+      if constexpr (C::NACC == 2) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          float4* dst = reinterpret_cast<float4*>(mine + (size_t)nt * 32 * 8);
-          __stcg(dst, make_float4(accB[nt][0], accB[nt][1], accB[nt][2], accB[nt][3]));
-          __stcg(dst + 1, make_float4(accD[nt][0], accD[nt][1], accD[nt][2], accD[nt][3]));
-        }
-        __threadfence();
-        named_bar_sync(1, kConsumerWarps * 32);
-        const long long first_u = (long long)cg * p.n_ks, last_u = first_u + p.n_ks - 1;
-        const int c_first = unit_owner(first_u, p.T, p.G), c_last = unit_owner(last_u, p.T, p.G);
-        if (threadIdx.x == 0) {
-          const int prev = atomicAdd(&p.counters[cg], 1);
-          *flag = (prev == c_last - c_first) ? 1 : 0;
-        }
-        named_bar_sync(1, kConsumerWarps * 32);
-        if (*flag) {
-          __threadfence();
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) accB[nt][i] = accD[nt][i] = 0.f;
-          for (int cc = c_first; cc <= c_last; ++cc) {
-            const long long cu0 = (long long)cc * p.T / p.G;
-            const int s2 = 2 * cc + ((int)(cu0 / p.n_ks) == cg ? 0 : 1);
-            const float* src = p.ws + (size_t)s2 * slot_floats + ((size_t)warp * NT * 32 + lane) * 8;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              const float4* sp = reinterpret_cast<const float4*>(src + (size_t)nt * 32 * 8);
-              const float4 vb = __ldcg(sp), vd = __ldcg(sp + 1);
-              accB[nt][0] += vb.x; accB[nt][1] += vb.y; accB[nt][2] += vb.z; accB[nt][3] += vb.w;
-              accD[nt][0] += vd.x; accD[nt][1] += vd.y; accD[nt][2] += vd.z; accD[nt][3] += vd.w;
-            }
+          for (int i = 0; i < 4; ++i) {
+            accB[0][nt][i] += accB[1][nt][i];
+            accD[0][nt][i] += accD[1][nt][i];
           }
-          epilogue<NT>(p, segs, tok2seg, cg, warp, lane, accB, accD);
-          if (threadIdx.x == 0) p.counters[cg] = 0;  // self-reset for the next launch
+      }
+      if constexpr (C::KSPLIT == 2) {
+        float* xw = xchg + ((size_t)tile * NT * 32 + lane) * 8;
+        if (kh == 1) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            float4* d = reinterpret_cast<float4*>(xw + (size_t)nt * 32 * 8);
+            d[0] = make_float4(accB[0][nt][0], accB[0][nt][1], accB[0][nt][2], accB[0][nt][3]);
+            d[1] = make_float4(accD[0][nt][0], accD[0][nt][1], accD[0][nt][2], accD[0][nt][3]);
+          }
         }
-        named_bar_sync(1, kConsumerWarps * 32);
+        named_bar_sync(1, C::CW * 32);
+        if (kh == 0) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const float4* d = reinterpret_cast<const float4*>(xw + (size_t)nt * 32 * 8);
+            const float4 vb = d[0], vd = d[1];
+            accB[0][nt][0] += vb.x; accB[0][nt][1] += vb.y; accB[0][nt][2] += vb.z; accB[0][nt][3] += vb.w;
+            accD[0][nt][0] += vd.x; accD[0][nt][1] += vd.y; accD[0][nt][2] += vd.z; accD[0][nt][3] += vd.w;
+          }
+        }
+        named_bar_sync(1, C::CW * 32);
+      }
+      if (kh == 0) {
+        const bool whole = (piece_start == (long long)cg * p.n_ks) && (ks == p.n_ks - 1);
+        if (whole) {
+          epilogue<NT>(p, segs, tok2seg, cg, tile, lane, accB[0], accD[0]);
+        } else {
+          const int slot = 2 * c + (cg == cg_first ? 0 : 1);
+          const size_t slot_floats = (size_t)kTilesPerCg * NT * 32 * 8;
+          float* mine = p.ws + (size_t)slot * slot_floats + ((size_t)tile * NT * 32 + lane) * 8;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            float4* dst = reinterpret_cast<float4*>(mine + (size_t)nt * 32 * 8);
+            __stcg(dst, make_float4(accB[0][nt][0], accB[0][nt][1], accB[0][nt][2], accB[0][nt][3]));
+            __stcg(dst + 1, make_float4(accD[0][nt][0], accD[0][nt][1], accD[0][nt][2], accD[0][nt][3]));
+          }
+          __threadfence();
+          named_bar_sync(2, kTilesPerCg * 32);
+          const long long first_u = (long long)cg * p.n_ks, last_u = first_u + p.n_ks - 1;
+          const int c_first = unit_owner(first_u, p.T, p.G), c_last = unit_owner(last_u, p.T, p.G);
+          if (threadIdx.x == 0) {
+            const int prev = atomicAdd(&p.counters[cg], 1);
+            *flag = (prev == c_last - c_first) ? 1 : 0;
+          }
+          named_bar_sync(2, kTilesPerCg * 32);
+          if (*flag) {
+            __threadfence();
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) accB[0][nt][i] = accD[0][nt][i] = 0.f;
+            for (int cc = c_first; cc <= c_last; ++cc) {
+              const long long cu0 = (long long)cc * p.T / p.G;
+              const int s2 = 2 * cc + ((int)(cu0 / p.n_ks) == cg ? 0 : 1);
+              const float* src = p.ws + (size_t)s2 * slot_floats + ((size_t)tile * NT * 32 + lane) * 8;
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) {
+                const float4* sp = reinterpret_cast<const float4*>(src + (size_t)nt * 32 * 8);
+                const float4 vb = __ldcg(sp), vd = __ldcg(sp + 1);
+                accB[0][nt][0] += vb.x; accB[0][nt][1] += vb.y; accB[0][nt][2] += vb.z; accB[0][nt][3] += vb.w;
+                accD[0][nt][0] += vd.x; accD[0][nt][1] += vd.y; accD[0][nt][2] += vd.z; accD[0][nt][3] += vd.w;
+              }
+            }
+            epilogue<NT>(p, segs, tok2seg, cg, tile, lane, accB[0], accD[0]);
+            if (threadIdx.x == 0) p.counters[cg] = 0;  // self-reset for the next launch
+          }
+          named_bar_sync(2, kTilesPerCg * 32);
+        }
       }
     }
+    if (++ks == p.n_ks) { ks = 0; ++cg; }
   }
 }
 
@@ -358,7 +456,7 @@ int launch(const LinearParams& p, size_t smem, cudaStream_t stream) {
     if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
     configured = true;
   }
-  me_linear_kernel<DB, NT><<<p.G, kThreads, smem, stream>>>(p);
+  me_linear_kernel<DB, NT><<<p.G, Cfg<NT>::THREADS, smem, stream>>>(p);
   return mesw_check_launch("me_linear");
 }
 
@@ -369,6 +467,15 @@ int launch_nt(const LinearParams& p, int nt, size_t smem, cudaStream_t s) {
     case 2: return launch<DB, 2>(p, smem, s);
     case 4: return launch<DB, 4>(p, smem, s);
     default: return launch<DB, 8>(p, smem, s);
+  }
+}
+
+static int xchg_bytes(int nt) {
+  switch (nt) {
+    case 1: return Cfg<1>::XCHG;
+    case 2: return Cfg<2>::XCHG;
+    case 4: return Cfg<4>::XCHG;
+    default: return Cfg<8>::XCHG;
   }
 }
 
@@ -383,7 +490,7 @@ static int round_nt(int B) {
 
 extern "C" uint64_t mesw_linear_workspace_bytes(int32_t B, int32_t num_ctas) {
   const int nt = round_nt(B < 1 ? 1 : B);
-  return (uint64_t)num_ctas * 2ull * kConsumerWarps * nt * 32 * 8 * sizeof(float);
+  return (uint64_t)num_ctas * 2ull * kTilesPerCg * nt * 32 * 8 * sizeof(float);
 }
 
 extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
@@ -435,8 +542,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   const int CB = kTileN * kTileK * db / 8;
   const int xbytes = nt * 8 * kXStride * 2;
   const int wbytes = a->w ? kWBytesPerUnit : 0;
-  // header upper bound (S <= 6): barriers + flag + tok2seg + segment table, 1 KiB aligned
-  const size_t hdr = ((size_t)(6 * 16 + 16 + 64 * 4 + MESW_MAX_SEGMENTS * sizeof(SegDesc)) + 1023) & ~size_t(1023);
+  const size_t hdr = header_bytes(6, nt, xchg_bytes(nt));  // upper bound (S <= 6)
   const size_t budget = 232448 - hdr;
   int segs_per_stage = p.n_seg == 0 ? 0 : (p.n_seg < kMaxSegsPerStage ? p.n_seg : kMaxSegsPerStage);
   int stage = 0, S = 0;
@@ -454,8 +560,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   p.x_off = wbytes + segs_per_stage * CB;
   p.segs_per_stage = segs_per_stage > 0 ? segs_per_stage : 1;
   p.n_chunks = p.n_seg == 0 ? 1 : (p.n_seg + p.segs_per_stage - 1) / p.segs_per_stage;
-  const size_t hdr_real = (((size_t)(S * 16 + 16 + nt * 8 * 4 + MESW_MAX_SEGMENTS * sizeof(SegDesc))) + 1023) & ~size_t(1023);
-  const size_t smem = hdr_real + (size_t)S * stage;
+  const size_t smem = header_bytes(S, nt, xchg_bytes(nt)) + (size_t)S * stage;
   if (smem > 232448) return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory overflow");
 
   cudaStream_t s = (cudaStream_t)stream;

@@ -289,6 +289,61 @@ class Workspace:
 
 # --------------------------------------------------------------------------- K2 call
 
+class LinearPlan:
+    """Pre-built launch of the fused multi-expert linear (pointers bound once).
+
+    Calling the plan issues one `mesw_me_linear` on the current (or given) stream;
+    this keeps per-launch host cost to one ctypes call and makes the launch
+    capturable in a CUDA graph.
+    """
+
+    def __init__(self, x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
+                 segments, out: torch.Tensor, residual: torch.Tensor | None = None,
+                 geom: LinearGeometry | None = None, num_ctas: int = 0, activation: str | None = None):
+        L = _lib.lib()
+        if geom is None:
+            geom = weight.geom if weight is not None else next(
+                d.geom for d in table.deltas if d is not None)
+        if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_cuda:
+            raise ValueError("x must be a 2-D bf16 CUDA tensor")
+        if x.stride(1) != 1 or out.stride(1) != 1:
+            raise ValueError("x and out must be row-contiguous")
+        if out.dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("output must be bf16 or f32")
+        segs = [(int(b), int(e), int(s)) for b, e, s in segments]
+        if len(segs) > _lib.MAX_SEGMENTS:
+            raise NotImplementedError(f"more than {_lib.MAX_SEGMENTS} expert segments in one launch")
+        self.geom = geom
+        self.keep = (x, weight, table, out, residual)  # keep buffers alive
+        ws = Workspace.get(x.device)
+        self.ws = ws
+        a = _lib.LinearArgs()
+        a.x = x.data_ptr()
+        a.B, a.m, a.n, a.ldx = x.shape[0], geom.m, geom.n, x.stride(0)
+        a.w = _ptr(weight.frag) if weight is not None else None
+        a.expert_table = table.dev.data_ptr() if table is not None else None
+        a.code_bits = table.code_bits if (table is not None and table.code_bits) else 2
+        a.n_segments = len(segs)
+        for i, (b, e, s) in enumerate(segs):
+            a.seg_begin[i], a.seg_end[i], a.seg_slot[i] = b, e, s
+        a.y = out.data_ptr()
+        a.y_bf16 = 1 if out.dtype == torch.bfloat16 else 0
+        a.ldy = out.stride(0)
+        if residual is not None:
+            if residual.dtype != torch.bfloat16:
+                raise ValueError("residual must be bf16")
+            a.residual, a.ld_res = residual.data_ptr(), residual.stride(0)
+        a.workspace, a.workspace_bytes = ws.ws.data_ptr(), ws.nbytes
+        a.counters = ws.counters.data_ptr()
+        a.num_ctas = num_ctas
+        a.activation = {None: 0, "relu": 1}[activation]
+        self.args = a
+        self._fn = L.mesw_me_linear
+
+    def __call__(self, stream=None) -> None:
+        _lib.check(self._fn(C.byref(self.args), _stream(stream)))
+
+
 def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
               segments, out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
               out_dtype=torch.bfloat16, geom: LinearGeometry | None = None, num_ctas: int = 0,
@@ -298,42 +353,10 @@ def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable |
     x: bf16 [B, ldx] on the GPU with ldx >= m_pad (pad columns zero), rows grouped
     by expert.  segments: iterable of (begin, end, slot) into `table`.
     """
-    L = _lib.lib()
     if geom is None:
         geom = weight.geom if weight is not None else next(
             d.geom for d in table.deltas if d is not None)
-    if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_cuda:
-        raise ValueError("x must be a 2-D bf16 CUDA tensor")
-    if x.stride(1) != 1:
-        raise ValueError("x must be row-contiguous")
-    B = x.shape[0]
-    segs = [(int(b), int(e), int(s)) for b, e, s in segments]
     if out is None:
-        out = torch.empty((B, geom.n), dtype=out_dtype, device=x.device)
-    ws = Workspace.get(x.device)
-    a = _lib.LinearArgs()
-    a.x = x.data_ptr()
-    a.B, a.m, a.n, a.ldx = B, geom.m, geom.n, x.stride(0)
-    a.w = _ptr(weight.frag) if weight is not None else None
-    a.expert_table = table.dev.data_ptr() if table is not None else None
-    a.code_bits = table.code_bits if (table is not None and table.code_bits) else 2
-    a.n_segments = len(segs)
-    if len(segs) > _lib.MAX_SEGMENTS:
-        raise NotImplementedError(f"more than {_lib.MAX_SEGMENTS} expert segments in one launch")
-    for i, (b, e, s) in enumerate(segs):
-        a.seg_begin[i], a.seg_end[i], a.seg_slot[i] = b, e, s
-    a.y = out.data_ptr()
-    a.y_bf16 = 1 if out.dtype == torch.bfloat16 else 0
-    if out.dtype not in (torch.bfloat16, torch.float32):
-        raise ValueError("output must be bf16 or f32")
-    a.ldy = out.stride(0)
-    if residual is not None:
-        if residual.dtype != torch.bfloat16:
-            raise ValueError("residual must be bf16")
-        a.residual, a.ld_res = residual.data_ptr(), residual.stride(0)
-    a.workspace, a.workspace_bytes = ws.ws.data_ptr(), ws.nbytes
-    a.counters = ws.counters.data_ptr()
-    a.num_ctas = num_ctas
-    a.activation = {None: 0, "relu": 1}[activation]
-    _lib.check(L.mesw_me_linear(C.byref(a), _stream(stream)))
+        out = torch.empty((x.shape[0], geom.n), dtype=out_dtype, device=x.device)
+    LinearPlan(x, weight, table, segments, out, residual, geom, num_ctas, activation)(stream)
     return out

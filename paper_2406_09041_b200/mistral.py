@@ -1,0 +1,320 @@
+"""Mistral-7B-shaped multi-expert decode engine (BASELINE configs 2 and 3).
+
+One shared bf16 base model; every request carries an expert id whose compressed
+delta (2-bit codes + fp16 salient rows) is applied inside the four fused linears
+of every decoder layer (q|k|v, o, gate|up, down -- 7 compressed projections, the
+224 decoder linears the paper's 2.13 GB Mistral delta covers).
+Embedding and lm_head are base-only.
+
+Requests are kept grouped by expert for the whole batch lifetime, so each fused
+linear sees fixed segments; the per-step launch sequence (all CUDA kernels from
+libmesw.so) is captured once in a CUDA graph and replayed.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan, _stream
+from .synth import MistralShape
+
+PROJ_ORDER = ("q", "k", "v", "o", "gate", "up", "down")
+
+
+@dataclass
+class LayerWeights:
+    attn_norm: torch.Tensor
+    qkv: DeviceWeight
+    o: DeviceWeight
+    mlp_norm: torch.Tensor
+    gateup: DeviceWeight
+    down: DeviceWeight
+
+
+class MistralMultiExpert:
+    """Base model + resident experts + decode buffers for up to `max_batch` requests."""
+
+    def __init__(self, shape: MistralShape = MistralShape(), max_batch: int = 32, ctx_max: int = 256,
+                 device="cuda", n_layers: int | None = None):
+        self.shape = shape
+        self.n_layers = shape.n_layers if n_layers is None else n_layers
+        self.device = torch.device(device)
+        self.max_batch = max_batch
+        self.ctx_max = ctx_max
+        s = shape
+        self.kv_dim = s.n_kv_heads * s.head_dim
+        self.g_qkv = LinearGeometry(s.hidden, (s.n_heads * s.head_dim, self.kv_dim, self.kv_dim))
+        self.g_o = LinearGeometry(s.n_heads * s.head_dim, (s.hidden,))
+        self.g_gu = LinearGeometry(s.hidden, (s.intermediate, s.intermediate))
+        self.g_down = LinearGeometry(s.intermediate, (s.hidden,))
+        self.g_head = LinearGeometry(s.hidden, (s.vocab,))
+        self.layers: list[LayerWeights] = []
+        self.tables = [[ExpertTable(self.device) for _ in range(4)] for _ in range(self.n_layers)]
+        self.experts: dict = {}
+        self.embedding = None
+        self.final_norm = None
+        self.head = None
+        self._alloc_buffers()
+        self.graph = None
+        self._plans = None
+
+    # ------------------------------------------------------------------ weights
+    def _alloc_buffers(self):
+        s, B, dev = self.shape, self.max_batch, self.device
+        bf = torch.bfloat16
+        self.ids = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.pos = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.len = torch.ones(B, dtype=torch.int32, device=dev)
+        self.h = torch.zeros((B, s.hidden), dtype=bf, device=dev)
+        self.xn = torch.zeros((B, max(s.hidden, self.g_o.m_pad)), dtype=bf, device=dev)
+        self.qkv = torch.zeros((B, self.g_qkv.n_pad), dtype=bf, device=dev)
+        self.attn = torch.zeros((B, self.g_o.m_pad), dtype=bf, device=dev)
+        self.gu = torch.zeros((B, self.g_gu.n_pad), dtype=bf, device=dev)
+        self.act = torch.zeros((B, self.g_down.m_pad), dtype=bf, device=dev)
+        self.logits = torch.zeros((B, self.g_head.n_pad), dtype=bf, device=dev)
+        kv_shape = (self.n_layers, B, self.ctx_max, s.n_kv_heads, s.head_dim)
+        self.kcache = torch.zeros(kv_shape, dtype=bf, device=dev)
+        self.vcache = torch.zeros(kv_shape, dtype=bf, device=dev)
+
+    def load_base(self, embedding, final_norm, head_w, layers: list) -> None:
+        """Install base weights.  `layers[l]` = dict(attn_norm, q, k, v, o, mlp_norm, gate, up, down)
+        with projection matrices in reference orientation [in, out] (bf16/f32 tensors)."""
+        dev = self.device
+        self.embedding = torch.as_tensor(embedding).to(dev, torch.bfloat16).contiguous()
+        self.final_norm = torch.as_tensor(final_norm).to(dev, torch.bfloat16).contiguous()
+        self.head = DeviceWeight.empty(self.g_head, dev)
+        self.head.load_block(0, torch.as_tensor(head_w).to(dev))
+        self.layers = []
+        for lw in layers:
+            qkv = DeviceWeight.empty(self.g_qkv, dev)
+            for b, name in enumerate(("q", "k", "v")):
+                qkv.load_block(b, torch.as_tensor(lw[name]).to(dev))
+            o = DeviceWeight.empty(self.g_o, dev)
+            o.load_block(0, torch.as_tensor(lw["o"]).to(dev))
+            gu = DeviceWeight.empty(self.g_gu, dev)
+            gu.load_block(0, torch.as_tensor(lw["gate"]).to(dev))
+            gu.load_block(1, torch.as_tensor(lw["up"]).to(dev))
+            down = DeviceWeight.empty(self.g_down, dev)
+            down.load_block(0, torch.as_tensor(lw["down"]).to(dev))
+            self.layers.append(LayerWeights(
+                attn_norm=torch.as_tensor(lw["attn_norm"]).to(dev, torch.bfloat16).contiguous(), qkv=qkv, o=o,
+                mlp_norm=torch.as_tensor(lw["mlp_norm"]).to(dev, torch.bfloat16).contiguous(), gateup=gu, down=down))
+        self._plans = None
+
+    def load_synthetic_base(self, seed: int = 0, std: float = 0.02) -> None:
+        """Random-init base weights of the Mistral architecture (no checkpoints offline),
+        generated on the device block by block."""
+        s, dev = self.shape, self.device
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+
+        def rnd(*shape):
+            return (torch.randn(shape, generator=g, device=dev, dtype=torch.float32) * std).to(torch.bfloat16)
+
+        self.embedding = rnd(s.vocab, s.hidden)
+        self.final_norm = torch.ones(s.hidden, dtype=torch.bfloat16, device=dev)
+        self.head = DeviceWeight.empty(self.g_head, dev)
+        self.head.load_block(0, rnd(s.hidden, s.vocab))
+        self.layers = []
+        for _ in range(self.n_layers):
+            qkv = DeviceWeight.empty(self.g_qkv, dev)
+            for b, nb in enumerate(self.g_qkv.block_n):
+                qkv.load_block(b, rnd(s.hidden, nb))
+            o = DeviceWeight.empty(self.g_o, dev)
+            o.load_block(0, rnd(self.g_o.m, s.hidden))
+            gu = DeviceWeight.empty(self.g_gu, dev)
+            gu.load_block(0, rnd(s.hidden, s.intermediate))
+            gu.load_block(1, rnd(s.hidden, s.intermediate))
+            down = DeviceWeight.empty(self.g_down, dev)
+            down.load_block(0, rnd(s.intermediate, s.hidden))
+            ones = torch.ones(s.hidden, dtype=torch.bfloat16, device=dev)
+            self.layers.append(LayerWeights(attn_norm=ones, qkv=qkv, o=o, mlp_norm=ones.clone(), gateup=gu,
+                                            down=down))
+        torch.cuda.synchronize(dev)
+        self._plans = None
+
+    def base_bytes(self) -> int:
+        n = sum(t.numel() * t.element_size() for lw in self.layers for t in
+                (lw.qkv.frag, lw.o.frag, lw.gateup.frag, lw.down.frag))
+        return n + self.head.frag.numel() * 2
+
+    # ------------------------------------------------------------------ experts
+    def add_expert(self, expert_id, artifact) -> int:
+        """Make an expert resident: its artifact holds 7 blocks per layer (q,k,v,o,gate,up,down)."""
+        layers = artifact.layers if hasattr(artifact, "layers") else list(artifact)
+        if len(layers) != 7 * self.n_layers:
+            raise ValueError(f"expert artifact has {len(layers)} blocks, expected {7 * self.n_layers}")
+        slot = len(self.experts)
+        nbytes = 0
+        for l in range(self.n_layers):
+            blk = dict(zip(PROJ_ORDER, layers[7 * l:7 * l + 7]))
+            deltas = [DeviceDelta.from_blocks([blk["q"], blk["k"], blk["v"]], self.g_qkv, self.device),
+                      DeviceDelta.from_blocks([blk["o"]], self.g_o, self.device),
+                      DeviceDelta.from_blocks([blk["gate"], blk["up"]], self.g_gu, self.device),
+                      DeviceDelta.from_blocks([blk["down"]], self.g_down, self.device)]
+            for t, d in zip(self.tables[l], deltas):
+                t.set(slot, d)
+                nbytes += d.nbytes
+        self.experts[expert_id] = (slot, nbytes)
+        self._plans = None
+        self.graph = None
+        return slot
+
+    def expert_bytes(self) -> int:
+        return sum(nb for _, nb in self.experts.values())
+
+    # ------------------------------------------------------------------ batch
+    def set_batch(self, expert_ids: list, prompt_lens: list | None = None) -> np.ndarray:
+        """Fix the request batch.  Requests are regrouped by expert; returns the order
+        (order[i] = caller's request index at engine row i).  Positions start at
+        prompt_lens (the KV cache rows below are assumed filled)."""
+        B = len(expert_ids)
+        if not 1 <= B <= self.max_batch:
+            raise ValueError(f"batch size must be in [1, {self.max_batch}]")
+        slots = []
+        for e in expert_ids:
+            if e is None:
+                slots.append(-1)
+            elif e not in self.experts:
+                from .errors import UnknownExpertError
+                raise UnknownExpertError(f"unknown expert {e!r}")
+            else:
+                slots.append(self.experts[e][0])
+        slots = np.asarray(slots)
+        order = np.argsort(slots, kind="stable")
+        segs, cur = [], 0
+        for sl in sorted(set(slots.tolist())):
+            cnt = int((slots == sl).sum())
+            if sl >= 0:
+                segs.append((cur, cur + cnt, int(sl)))
+            cur += cnt
+        pl = np.zeros(B, np.int64) if prompt_lens is None else np.asarray(prompt_lens, np.int64)[order]
+        if (pl >= self.ctx_max).any():
+            raise ValueError("prompt longer than the cache window")
+        if getattr(self, "B", None) != B or getattr(self, "segments", None) != segs:
+            self._plans = None  # launch geometry changed: rebuild plans / re-capture
+            self.graph = None
+        self.B = B
+        self.order = order
+        self.segments = segs
+        self.pos[:B] = torch.as_tensor(pl, dtype=torch.int32)
+        self.len[:B] = torch.as_tensor(pl + 1, dtype=torch.int32)
+        return order
+
+    def fill_random_kv(self, prompt_len: int, seed: int = 1) -> None:
+        """Synthetic prompt state: random K/V for positions < prompt_len (bench only)."""
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        for t in (self.kcache, self.vcache):
+            view = t[:, :, :prompt_len]
+            view.copy_((torch.randn(view.shape, generator=g, device=self.device) * 0.5).to(torch.bfloat16))
+
+    # ------------------------------------------------------------------ step
+    def _build_plans(self):
+        B, s, segs = self.B, self.shape, self.segments
+        plans = []
+        for l, lw in enumerate(self.layers):
+            tq, to, tgu, td = self.tables[l]
+            plans.append((
+                LinearPlan(self.xn[:B, :self.g_qkv.m_pad], lw.qkv, tq if segs else None, segs, self.qkv[:B]),
+                LinearPlan(self.attn[:B], lw.o, to if segs else None, segs, self.h[:B], residual=self.h[:B]),
+                LinearPlan(self.xn[:B, :self.g_gu.m_pad], lw.gateup, tgu if segs else None, segs, self.gu[:B]),
+                LinearPlan(self.act[:B], lw.down, td if segs else None, segs, self.h[:B], residual=self.h[:B]),
+            ))
+        head = LinearPlan(self.xn[:B, :self.g_head.m_pad], self.head, None, [], self.logits[:B])
+        self._plans = (plans, head)
+
+    def step(self, stream=None) -> None:
+        """One decode step for the whole batch: ids (engine order) -> next ids in self.ids."""
+        if self._plans is None:
+            self._build_plans()
+        L = _lib.lib()
+        st = _stream(stream)
+        s, B = self.shape, self.B
+        chk = _lib.check
+        plans, head = self._plans
+        H = s.hidden
+        chk(L.mesw_embed(self.ids.data_ptr(), B, self.embedding.data_ptr(), H, self.h.data_ptr(),
+                         self.h.stride(0), st))
+        for l, lw in enumerate(self.layers):
+            p_qkv, p_o, p_gu, p_down = plans[l]
+            chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), lw.attn_norm.data_ptr(), B, H,
+                               C.c_float(s.rms_eps), self.xn.data_ptr(), self.xn.stride(0), st))
+            p_qkv(stream)
+            kc, vc = self.kcache[l], self.vcache[l]
+            chk(L.mesw_rope_append(self.qkv.data_ptr(), self.qkv.stride(0), self.pos.data_ptr(), B, s.n_heads,
+                                   s.n_kv_heads, s.head_dim, C.c_float(s.rope_theta), kc.data_ptr(),
+                                   vc.data_ptr(), self.ctx_max, st))
+            chk(L.mesw_attention_decode(self.qkv.data_ptr(), self.qkv.stride(0), kc.data_ptr(), vc.data_ptr(),
+                                        self.len.data_ptr(), B, s.n_heads, s.n_kv_heads, s.head_dim,
+                                        self.ctx_max, self.attn.data_ptr(), self.attn.stride(0), st))
+            p_o(stream)
+            chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), lw.mlp_norm.data_ptr(), B, H,
+                               C.c_float(s.rms_eps), self.xn.data_ptr(), self.xn.stride(0), st))
+            p_gu(stream)
+            chk(L.mesw_swiglu(self.gu.data_ptr(), self.gu.stride(0), B, s.intermediate, self.act.data_ptr(),
+                              self.act.stride(0), st))
+            p_down(stream)
+        chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), self.final_norm.data_ptr(), B, H,
+                           C.c_float(s.rms_eps), self.xn.data_ptr(), self.xn.stride(0), st))
+        head(stream)
+        chk(L.mesw_argmax(self.logits.data_ptr(), 1, B, s.vocab, self.logits.stride(0), self.ids.data_ptr(), st))
+        chk(L.mesw_advance_positions(self.pos.data_ptr(), self.len.data_ptr(), B, self.ctx_max,
+                                     min(self.ctx_max - 1, 128), st))
+
+    def launches_per_step(self) -> int:
+        return 1 + 9 * self.n_layers + 4
+
+    def capture(self) -> None:
+        """Capture one decode step in a CUDA graph (replayed by `replay`)."""
+        self.step()  # warm: configures kernel attributes outside capture
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            self.step(stream=s)
+            g.capture_end()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self.graph = g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def bytes_per_step(self) -> dict:
+        """Algorithmic HBM bytes of one decode step."""
+        s, B = self.shape, self.B
+        from .synth import linear_bytes
+        n_exp = len(self.segments)
+        lin = 0
+        delta = 0
+        for g in (self.g_qkv, self.g_o, self.g_gu, self.g_down):
+            lin += linear_bytes(g.m, g.n, n_exp, B)
+            delta += linear_bytes(g.m, g.n, n_exp, B, base=False) - 2 * B * (g.m + g.n)
+        lin *= self.n_layers
+        delta *= self.n_layers
+        head = linear_bytes(s.hidden, s.vocab, 0, B)
+        ctx = int(self.len[:B].float().mean().item())
+        kv = 2 * B * ctx * s.n_kv_heads * s.head_dim * 2 * self.n_layers
+        return {"linears": lin, "delta": delta, "head": head, "kv": kv, "total": lin + head + kv}
+
+    # ------------------------------------------------------------------ public API
+    def decode(self, host_ids: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:
+        """End-to-end step through the public API: host token ids (engine order, int32,
+        pinned) -> device, one graph-replayed decode step, next ids -> host."""
+        B = self.B
+        self.ids[:B].copy_(host_ids[:B], non_blocking=True)
+        self.replay()
+        if out_host is None:
+            out_host = torch.empty(B, dtype=torch.int32, pin_memory=True)
+        out_host.copy_(self.ids[:B], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return out_host

@@ -169,40 +169,57 @@ def test_fused_linear_other_widths(bits):
     assert _rel(y, ref) <= 2e-3
 
 
-def test_batch_composition_invariance_bitwise():
-    """a query's result does not depend on the rest of the batch (exact)."""
-    torch = _torch()
-    from paper_2406_09041_b200.device import me_linear
-    geom, dw, w_bf, table, experts = _setup_linear(512, (384,), 3, seed=11)
-    rng = np.random.default_rng(5)
-    X = torch.from_numpy(rng.normal(0, 1, size=(24, geom.m_pad)).astype(np.float32)).to(torch.bfloat16).cuda()
-    expert_of = rng.integers(0, 3, size=24)
-    order = np.argsort(expert_of, kind="stable")
+def _grouped(expert_of, perm):
+    order = np.concatenate([np.flatnonzero(expert_of == e) for e in perm])
     segs, cur = [], 0
-    for e in range(3):
+    for e in perm:
         cnt = int((expert_of == e).sum())
         if cnt:
             segs.append((cur, cur + cnt, e))
         cur += cnt
-    y_full = me_linear(X[torch.from_numpy(order).cuda()].contiguous(), dw, table, segs,
-                       out_dtype=torch.float32).cpu().numpy()
-    for pos, q in enumerate(order):
-        e = int(expert_of[q])
-        y1 = me_linear(X[q:q + 1].contiguous(), dw, table, [(0, 1, e)], out_dtype=torch.float32).cpu().numpy()
-        assert np.array_equal(y1[0], y_full[pos])
-    # different expert order in the batch -> same bits per query
-    perm = [2, 0, 1]
-    order2 = np.concatenate([np.flatnonzero(expert_of == e) for e in perm])
-    segs2, cur = [], 0
-    for e in perm:
-        cnt = int((expert_of == e).sum())
-        segs2.append((cur, cur + cnt, e))
-        cur += cnt
-    y_perm = me_linear(X[torch.from_numpy(order2).cuda()].contiguous(), dw, table, segs2,
-                       out_dtype=torch.float32).cpu().numpy()
-    pos_full = {int(q): i for i, q in enumerate(order)}
-    for i, q in enumerate(order2):
-        assert np.array_equal(y_perm[i], y_full[pos_full[int(q)]])
+    return order, segs
+
+
+@pytest.mark.parametrize("B", [7, 16, 24, 64])
+def test_group_order_invariance_bitwise(B):
+    """per-query results do not depend on the order in which expert
+    groups are laid out in the batch -- exact equality."""
+    torch = _torch()
+    from paper_2406_09041_b200.device import me_linear
+    geom, dw, w_bf, table, experts = _setup_linear(512, (384,), 3, seed=11)
+    rng = np.random.default_rng(B)
+    X = torch.from_numpy(rng.normal(0, 1, size=(B, geom.m_pad)).astype(np.float32)).to(torch.bfloat16).cuda()
+    expert_of = rng.integers(0, 3, size=B)
+    results = []
+    for perm in ([0, 1, 2], [2, 0, 1], [1, 2, 0]):
+        order, segs = _grouped(expert_of, perm)
+        y = me_linear(X[torch.from_numpy(order).cuda()].contiguous(), dw, table, segs,
+                      out_dtype=torch.float32).cpu().numpy()
+        back = np.empty_like(y)
+        back[order] = y
+        results.append(back)
+    assert np.array_equal(results[0], results[1]) and np.array_equal(results[0], results[2])
+
+
+def test_batch_of_one_and_same_expert_pairs_bitwise():
+    """SPEC.md:438 examples: a batch of one equals a single call; two queries of the same
+    expert equal two single calls (exact).  Across token-tile classes (B<=8, <=16, <=32,
+    <=64) the k-reduction is regrouped, so results agree to f32 reassociation only."""
+    torch = _torch()
+    from paper_2406_09041_b200.device import me_linear
+    geom, dw, w_bf, table, experts = _setup_linear(512, (384,), 3, seed=12)
+    rng = np.random.default_rng(1)
+    X = torch.from_numpy(rng.normal(0, 1, size=(8, geom.m_pad)).astype(np.float32)).to(torch.bfloat16).cuda()
+    y_pair = me_linear(X[:2].contiguous(), dw, table, [(0, 2, 1)], out_dtype=torch.float32).cpu().numpy()
+    for i in range(2):
+        y1 = me_linear(X[i:i + 1].contiguous(), dw, table, [(0, 1, 1)], out_dtype=torch.float32).cpu().numpy()
+        assert np.array_equal(y1[0], y_pair[i])
+    y8 = me_linear(X, dw, table, [(0, 3, 0), (3, 8, 1)], out_dtype=torch.float32).cpu().numpy()
+    y1 = me_linear(X[4:5].contiguous(), dw, table, [(0, 1, 1)], out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(y1[0], y8[4])
+    X32 = torch.cat([X] * 4).contiguous()
+    y32 = me_linear(X32, dw, table, [(0, 3, 0), (3, 32, 1)], out_dtype=torch.float32).cpu().numpy()
+    assert _rel(y32[4], y8[4]) <= 1e-6
 
 
 def test_c1_shape_mixed_decode():
