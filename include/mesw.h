@@ -150,8 +150,9 @@ typedef struct {
 } mesw_expert_dev;
 
 typedef struct {
-  const uint16_t* x;  /* bf16 [B][ldx]; columns m..m_pad-1 must be 0          */
-  int32_t B, m, n, ldx;
+  const uint16_t* x;  /* bf16 activations, canonical tile layout (mesw_pack_x)  */
+  int32_t B, m, n;
+  int32_t x_layout;   /* must be 0 (canonical)                                 */
   const uint16_t* w;  /* fragment-layout bf16 base, or NULL (delta only)      */
   const mesw_expert_dev* expert_table; /* DEVICE array indexed by slot        */
   int32_t code_bits;  /* 2, 4 or 8: shared by all experts of the launch       */
@@ -171,10 +172,23 @@ typedef struct {
   int32_t activation; /* 0: none, 1: ReLU (toylm.py:207), applied last         */
 } mesw_linear_args;
 
+/* Canonical activation layout consumed by mesw_me_linear: rows padded to
+ * NP = ceil16(B); for each 128-wide k-step ks a tile of NP*128 bf16 laid out as
+ * [NP/8 row groups][16 k-chunks][8 rows][8 elems] (the UMMA K-major SWIZZLE_NONE
+ * canonical B operand), so one bulk copy stages it:
+ *   index(t, k) = (k/128)*NP*128 + (t/8)*1024 + ((k%128)/8)*64 + (t%8)*8 + k%8.
+ * Rows >= B and columns >= m are written as 0. */
+int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t* d_xc, void* stream);
+/* Inverse (debug / tests): canonical -> row-major [B][ldy]. */
+int mesw_unpack_x(const uint16_t* d_xc, int B, int m, uint16_t* d_y, int ldy, void* stream);
+
 /* Workspace bytes mesw_me_linear needs for a given B and CTA count. */
 uint64_t mesw_linear_workspace_bytes(int32_t B, int32_t num_ctas);
 int mesw_me_linear(const mesw_linear_args* args, void* stream);
 
+/* Glue outputs: row-major with leading dimension ld, or -- when *_np > 0 -- the
+ * canonical activation layout (see mesw_pack_x) with NP = *_np rows, ready to be
+ * the x operand of the next fused linear. */
 /* ------------------------------------- K5: Mistral decoder glue (decode step)
  * The reference toy model has no attention (toylm.py:1-8); these are the
  * standard decoder pieces around the fused linears of the Mistral-shaped
@@ -184,7 +198,7 @@ int mesw_embed(const int32_t* d_ids, int B, const uint16_t* d_table, int H, uint
                int ld_out, void* stream);
 /* y = x * rsqrt(mean(x^2) + eps) * w */
 int mesw_rmsnorm(const uint16_t* d_x, int ldx, const uint16_t* d_w, int B, int H, float eps,
-                 uint16_t* d_y, int ldy, void* stream);
+                 uint16_t* d_y, int ldy, int y_np, void* stream);
 /* RoPE (rotate-half) on the q and k heads of a fused qkv row, append k/v to the
  * caches [B][ctx_max][n_kv][head_dim] at position pos[b]. */
 int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_pos, int B, int n_heads,
@@ -194,10 +208,10 @@ int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_pos, int B, i
 int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
                           const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
                           int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
-                          void* stream);
+                          int out_np, void* stream);
 /* out = silu(gate) * up for rows [gate(I) | up(I)]. */
 int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,
-                void* stream);
+                int out_np, void* stream);
 /* Greedy next token: argmax with ties to the lowest id (toylm.py:247). */
 int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int ld, int32_t* d_out,
                 void* stream);

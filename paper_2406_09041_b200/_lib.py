@@ -30,7 +30,7 @@ class ExpertDev(C.Structure):
 
 class LinearArgs(C.Structure):
     _fields_ = [("x", C.c_void_p), ("B", C.c_int32), ("m", C.c_int32), ("n", C.c_int32),
-                ("ldx", C.c_int32), ("w", C.c_void_p), ("expert_table", C.c_void_p),
+                ("x_layout", C.c_int32), ("w", C.c_void_p), ("expert_table", C.c_void_p),
                 ("code_bits", C.c_int32), ("n_segments", C.c_int32),
                 ("seg_begin", C.c_int32 * MAX_SEGMENTS), ("seg_end", C.c_int32 * MAX_SEGMENTS),
                 ("seg_slot", C.c_int32 * MAX_SEGMENTS), ("y", C.c_void_p), ("y_bf16", C.c_int32),
@@ -65,16 +65,20 @@ _SIGNATURES = [
                                      C.c_void_p]),
     ("mesw_unpack_weight_debug", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                            C.c_uint32, C.c_void_p, C.c_void_p]),
+    ("mesw_pack_x", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    ("mesw_unpack_x", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_linear_workspace_bytes", C.c_uint64, [C.c_int32, C.c_int32]),
     ("mesw_me_linear", C.c_int, [C.POINTER(LinearArgs), C.c_void_p]),
     ("mesw_embed", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_rmsnorm", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p,
-                               C.c_int, C.c_void_p]),
+                               C.c_int, C.c_int, C.c_void_p]),
     ("mesw_rope_append", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_float, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_attention_decode", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
-                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
-    ("mesw_swiglu", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
+                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                                        C.c_void_p]),
+    ("mesw_swiglu", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                              C.c_void_p]),
     ("mesw_argmax", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     ("mesw_advance_positions", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
 ]

@@ -13,6 +13,16 @@
 
 namespace mesw {
 
+// Canonical activation layout of mesw.h (consumed by the fused linear).
+__device__ __forceinline__ size_t canon_index(int t, int k, int NP) {
+  return (size_t)(k >> 7) * NP * 128 + (size_t)(t >> 3) * 1024 + ((k & 127) >> 3) * 64 + (t & 7) * 8 + (k & 7);
+}
+
+// Output address of element (t, k): row-major with ld, or canonical when np > 0.
+__device__ __forceinline__ size_t out_index(int t, int k, int ld, int np) {
+  return np > 0 ? canon_index(t, k, np) : (size_t)t * ld + k;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -54,25 +64,46 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __
   for (int i = threadIdx.x; i < H / 8; i += blockDim.x) dst[i] = src[i];
 }
 
-// y = x * rsqrt(mean(x^2) + eps) * w   (one CTA per token)
-__global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, int ldx, const uint16_t* __restrict__ w,
-                               int H, float eps, uint16_t* __restrict__ y, int ldy) {
+// y = x * rsqrt(mean(x^2) + eps) * w   (one CTA per token; row held in registers,
+// one 16-byte load per 8 elements, single global pass)
+constexpr int kNormThreads = 256;
+constexpr int kNormMaxVec = 4;  // up to 256 * 4 * 8 = 8192 channels
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* __restrict__ x, int ldx,
+                                                               const uint16_t* __restrict__ w, int H, float eps,
+                                                               uint16_t* __restrict__ y, int ldy, int ynp) {
   __shared__ float red[32];
-  const uint16_t* xr = x + (size_t)blockIdx.x * ldx;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)blockIdx.x * ldx);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const int nvec = H / 8;
+  uint4 v[kNormMaxVec];
   float ss = 0.f;
-  for (int i = threadIdx.x * 2; i < H; i += blockDim.x * 2) {
-    const uint32_t v = *reinterpret_cast<const uint32_t*>(xr + i);
-    const float a = bf16_lo(v), b = bf16_hi(v);
-    ss = fmaf(a, a, fmaf(b, b, ss));
+#pragma unroll
+  for (int j = 0; j < kNormMaxVec; ++j) {
+    const int i = threadIdx.x + j * kNormThreads;
+    if (i < nvec) {
+      v[j] = xr[i];
+      const uint32_t* e = reinterpret_cast<const uint32_t*>(&v[j]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ss = fmaf(bf16_lo(e[q]), bf16_lo(e[q]), fmaf(bf16_hi(e[q]), bf16_hi(e[q]), ss));
+    }
   }
-  const float tot = block_sum(ss, red);
-  const float r = rsqrtf(tot / (float)H + eps);
-  uint16_t* yr = y + (size_t)blockIdx.x * ldy;
-  for (int i = threadIdx.x * 2; i < H; i += blockDim.x * 2) {
-    const uint32_t v = *reinterpret_cast<const uint32_t*>(xr + i);
-    const uint32_t g = *reinterpret_cast<const uint32_t*>(w + i);
-    __nv_bfloat162 o = __floats2bfloat162_rn(bf16_lo(v) * r * bf16_lo(g), bf16_hi(v) * r * bf16_hi(g));
-    *reinterpret_cast<__nv_bfloat162*>(yr + i) = o;
+  const float r = rsqrtf(block_sum(ss, red) / (float)H + eps);
+#pragma unroll
+  for (int j = 0; j < kNormMaxVec; ++j) {
+    const int i = threadIdx.x + j * kNormThreads;
+    if (i < nvec) {
+      const uint4 g4 = wr[i];
+      const uint32_t* e = reinterpret_cast<const uint32_t*>(&v[j]);
+      const uint32_t* g = reinterpret_cast<const uint32_t*>(&g4);
+      uint4 o;
+      uint32_t* oo = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(bf16_lo(e[q]) * r * bf16_lo(g[q]), bf16_hi(e[q]) * r * bf16_hi(g[q]));
+        oo[q] = *reinterpret_cast<uint32_t*>(&t);
+      }
+      *reinterpret_cast<uint4*>(y + out_index(blockIdx.x, i * 8, ldy, ynp)) = o;
+    }
   }
 }
 
@@ -108,83 +139,128 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int ld_qkv, const
   }
 }
 
-// GQA decode attention: one CTA per (token, kv head); G = n_heads / n_kv query heads
-// share the kv head.  scores in smem (f32), softmax per head, then P.V.
-// block = D threads (D = 128), dynamic smem = G * ctx_max floats + G*D floats.
+// GQA decode attention: one CTA per (token, kv head); the G = n_heads / n_kv query
+// heads sharing the kv head are processed together.  K and V rows of the context
+// are staged in shared memory with coalesced 16-byte loads (rows padded to 272 B:
+// conflict-free 128-bit accesses), then
+//   scores: thread t owns position t (all G heads, 128-dim dot from smem),
+//   softmax: block reductions per head (fixed order),
+//   P.V: thread = (4-dim group, position slice), slices reduced through smem.
+// D must be 128; L <= kAttnMaxCtx.
+constexpr int kAttnThreads = 256;
+constexpr int kAttnMaxCtx = 320;
+constexpr int kAttnRow = 136;  // bf16 per staged row (128 + 8 pad)
+
 template <int G>
-__global__ void attn_decode_kernel(const uint16_t* __restrict__ q, int ld_q, const uint16_t* __restrict__ kc,
-                                   const uint16_t* __restrict__ vc, const int32_t* __restrict__ len,
-                                   int n_kv, int D, int ctx_max, float scale, uint16_t* __restrict__ out,
-                                   int ld_out) {
-  extern __shared__ float sm[];
+__global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(
+    const uint16_t* __restrict__ q, int ld_q, const uint16_t* __restrict__ kc, const uint16_t* __restrict__ vc,
+    const int32_t* __restrict__ len, int n_kv, int ctx_max, float scale, uint16_t* __restrict__ out, int ld_out,
+    int out_np) {
+  constexpr int D = 128;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  uint16_t* Ks = reinterpret_cast<uint16_t*>(smraw);                  // [L][136]
+  uint16_t* Vs = Ks + (size_t)kAttnMaxCtx * kAttnRow;                 // [L][136]
+  float* qs = reinterpret_cast<float*>(Vs + (size_t)kAttnMaxCtx * kAttnRow);  // [G][D]
+  float* ps = qs + G * D;                                             // [L][G] probabilities
+  float* part = ps + kAttnMaxCtx * G;                                 // [8 slices][G][D]
   __shared__ float red[32];
   const int b = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
   const int L = len[b];
-  float* qs = sm;                 // [G][D]
-  float* sc = sm + G * D;         // [G][ctx_max]
-  for (int i = tid; i < G * D; i += blockDim.x) {
-    const int hh = i / D, d = i % D;
-    qs[i] = bf16_to_f32(q[(size_t)b * ld_q + (size_t)(g * G + hh) * D + d]) * scale;
-  }
-  __syncthreads();
   const size_t kv_stride = (size_t)n_kv * D;
   const uint16_t* kb = kc + ((size_t)b * ctx_max * n_kv + g) * D;
   const uint16_t* vb = vc + ((size_t)b * ctx_max * n_kv + g) * D;
-  // scores: warp per position, lanes over D
-  const int lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
-  for (int t = w; t < L; t += nw) {
-    const uint16_t* kr = kb + (size_t)t * kv_stride;
+  // stage K, V (16 chunks of 16 B per row)
+  for (int i = tid; i < L * 16; i += kAttnThreads) {
+    const int t = i >> 4, c = i & 15;
+    *reinterpret_cast<uint4*>(Ks + t * kAttnRow + c * 8) = *reinterpret_cast<const uint4*>(kb + t * kv_stride + c * 8);
+    *reinterpret_cast<uint4*>(Vs + t * kAttnRow + c * 8) = *reinterpret_cast<const uint4*>(vb + t * kv_stride + c * 8);
+  }
+  for (int i = tid; i < G * D; i += kAttnThreads)
+    qs[i] = bf16_to_f32(q[(size_t)b * ld_q + (size_t)g * G * D + i]) * scale;
+  __syncthreads();
+  // scores
+  float sc[G];
+  float mx[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) { sc[h] = -INFINITY; }
+  for (int t = tid; t < L; t += kAttnThreads) {
     float acc[G];
 #pragma unroll
-    for (int hh = 0; hh < G; ++hh) acc[hh] = 0.f;
-    for (int d = lane * 2; d < D; d += 64) {
-      const uint32_t kv2 = *reinterpret_cast<const uint32_t*>(kr + d);
-      const float k0 = bf16_lo(kv2), k1 = bf16_hi(kv2);
+    for (int h = 0; h < G; ++h) acc[h] = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < 16; ++c) {
+      const uint4 k4 = *reinterpret_cast<const uint4*>(Ks + t * kAttnRow + c * 8);
+      const uint32_t* kk = reinterpret_cast<const uint32_t*>(&k4);
 #pragma unroll
-      for (int hh = 0; hh < G; ++hh) acc[hh] = fmaf(qs[hh * D + d], k0, fmaf(qs[hh * D + d + 1], k1, acc[hh]));
+      for (int h = 0; h < G; ++h) {
+        const float4 qa = *reinterpret_cast<const float4*>(qs + h * D + c * 8);
+        const float4 qb = *reinterpret_cast<const float4*>(qs + h * D + c * 8 + 4);
+        float a = acc[h];
+        a = fmaf(qa.x, bf16_lo(kk[0]), a); a = fmaf(qa.y, bf16_hi(kk[0]), a);
+        a = fmaf(qa.z, bf16_lo(kk[1]), a); a = fmaf(qa.w, bf16_hi(kk[1]), a);
+        a = fmaf(qb.x, bf16_lo(kk[2]), a); a = fmaf(qb.y, bf16_hi(kk[2]), a);
+        a = fmaf(qb.z, bf16_lo(kk[3]), a); a = fmaf(qb.w, bf16_hi(kk[3]), a);
+        acc[h] = a;
+      }
     }
 #pragma unroll
-    for (int hh = 0; hh < G; ++hh) {
-      const float s = warp_sum(acc[hh]);
-      if (lane == 0) sc[hh * ctx_max + t] = s;
-    }
+    for (int h = 0; h < G; ++h) { ps[t * G + h] = acc[h]; }
   }
   __syncthreads();
-  // softmax per head (block-wide, fixed order)
-  for (int hh = 0; hh < G; ++hh) {
-    float mx = -INFINITY;
-    for (int t = tid; t < L; t += blockDim.x) mx = fmaxf(mx, sc[hh * ctx_max + t]);
-    mx = block_max(mx, red);
-    float sum = 0.f;
-    for (int t = tid; t < L; t += blockDim.x) {
-      const float e = __expf(sc[hh * ctx_max + t] - mx);
-      sc[hh * ctx_max + t] = e;
-      sum += e;
-    }
-    sum = block_sum(sum, red);
-    const float inv = 1.f / sum;
-    for (int t = tid; t < L; t += blockDim.x) sc[hh * ctx_max + t] *= inv;
-    __syncthreads();
+  // softmax per head
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float m = -INFINITY;
+    for (int t = tid; t < L; t += kAttnThreads) m = fmaxf(m, ps[t * G + h]);
+    mx[h] = block_max(m, red);
   }
-  // out[h][d] = sum_t p[h][t] v[t][d]; thread = dim d
-  for (int d = tid; d < D; d += blockDim.x) {
-    float acc[G];
+  float sum[G];
 #pragma unroll
-    for (int hh = 0; hh < G; ++hh) acc[hh] = 0.f;
-    for (int t = 0; t < L; ++t) {
-      const float vv = bf16_to_f32(vb[(size_t)t * kv_stride + d]);
+  for (int h = 0; h < G; ++h) sum[h] = 0.f;
+  for (int t = tid; t < L; t += kAttnThreads) {
 #pragma unroll
-      for (int hh = 0; hh < G; ++hh) acc[hh] = fmaf(sc[hh * ctx_max + t], vv, acc[hh]);
+    for (int h = 0; h < G; ++h) {
+      const float e = __expf(ps[t * G + h] - mx[h]);
+      ps[t * G + h] = e;
+      sum[h] += e;
     }
+  }
 #pragma unroll
-    for (int hh = 0; hh < G; ++hh)
-      out[(size_t)b * ld_out + (size_t)(g * G + hh) * D + d] = __bfloat16_as_ushort(__float2bfloat16_rn(acc[hh]));
+  for (int h = 0; h < G; ++h) sc[h] = 1.f / block_sum(sum[h], red);
+  __syncthreads();
+  // P.V: thread = (dim group dg of 4 dims, slice sl of positions)
+  const int dg = tid & 31, sl = tid >> 5;  // 32 groups x 8 slices
+  float o[G][4];
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[h][j] = 0.f;
+  for (int t = sl; t < L; t += 8) {
+    const uint2 v2 = *reinterpret_cast<const uint2*>(Vs + t * kAttnRow + dg * 4);
+    const float v0 = bf16_lo(v2.x), v1 = bf16_hi(v2.x), v2f = bf16_lo(v2.y), v3 = bf16_hi(v2.y);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float p = ps[t * G + h];
+      o[h][0] = fmaf(p, v0, o[h][0]); o[h][1] = fmaf(p, v1, o[h][1]);
+      o[h][2] = fmaf(p, v2f, o[h][2]); o[h][3] = fmaf(p, v3, o[h][3]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+    *reinterpret_cast<float4*>(part + ((size_t)sl * G + h) * D + dg * 4) = make_float4(o[h][0], o[h][1], o[h][2], o[h][3]);
+  __syncthreads();
+  for (int i = tid; i < G * D; i += kAttnThreads) {
+    const int h = i / D, d = i % D;
+    float acc = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) acc += part[((size_t)s2 * G + h) * D + d];
+    out[out_index(b, (g * G + h) * D + d, ld_out, out_np)] = __bfloat16_as_ushort(__float2bfloat16_rn(acc * sc[h]));
   }
 }
 
 // out = silu(gate) * up, gate/up halves of a [B][2I] row.
 __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int ld_gu, int I, uint16_t* __restrict__ out,
-                              int ld_out) {
+                              int ld_out, int out_np) {
   const int b = blockIdx.y;
   const uint16_t* r = gu + (size_t)b * ld_gu;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2; i < I; i += gridDim.x * blockDim.x * 2) {
@@ -192,7 +268,7 @@ __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int ld_gu, int I,
     const uint32_t u2 = *reinterpret_cast<const uint32_t*>(r + I + i);
     const float g0 = bf16_lo(g2), g1 = bf16_hi(g2);
     const float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
-    *reinterpret_cast<__nv_bfloat162*>(out + (size_t)b * ld_out + i) =
+    *reinterpret_cast<__nv_bfloat162*>(out + out_index(b, i, ld_out, out_np)) =
         __floats2bfloat162_rn(s0 * bf16_lo(u2), s1 * bf16_hi(u2));
   }
 }
@@ -233,6 +309,39 @@ __global__ void argmax_kernel(const void* __restrict__ logits, int is_bf16, int 
   }
 }
 
+// Row-major -> canonical (one thread per 16-byte chunk of 8 k); zero padding.
+__global__ void pack_x_kernel(const uint16_t* __restrict__ x, int B, int m, int ldx, uint16_t* __restrict__ xc,
+                              int NP, int n_ks) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)n_ks * NP * 16;
+  if (tid >= total) return;
+  const int kc = (int)(tid % 16);
+  const int t = (int)((tid / 16) % NP);
+  const int ks = (int)(tid / (16LL * NP));
+  const int k0 = ks * 128 + kc * 8;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (t < B) {
+    if (k0 + 8 <= m && (ldx % 8) == 0) {
+      v = *reinterpret_cast<const uint4*>(x + (size_t)t * ldx + k0);
+    } else {
+      uint16_t e[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) e[i] = (k0 + i < m) ? x[(size_t)t * ldx + k0 + i] : (uint16_t)0;
+      v = make_uint4(e[0] | (uint32_t(e[1]) << 16), e[2] | (uint32_t(e[3]) << 16), e[4] | (uint32_t(e[5]) << 16),
+                     e[6] | (uint32_t(e[7]) << 16));
+    }
+  }
+  *reinterpret_cast<uint4*>(xc + canon_index(t, k0, NP)) = v;
+}
+
+__global__ void unpack_x_kernel(const uint16_t* __restrict__ xc, int B, int m, int NP, uint16_t* __restrict__ y,
+                                int ldy) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)B * m) return;
+  const int t = (int)(tid / m), k = (int)(tid % m);
+  y[(size_t)t * ldy + k] = xc[canon_index(t, k, NP)];
+}
+
 // Advance every request by one position (pos += 1, len = pos + 1); a request that
 // reaches the end of its cache window wraps back to `wrap_to` (bench steady state).
 __global__ void advance_kernel(int32_t* __restrict__ pos, int32_t* __restrict__ len, int B, int ctx_max,
@@ -264,9 +373,11 @@ extern "C" int mesw_embed(const int32_t* d_ids, int B, const uint16_t* d_table, 
 }
 
 extern "C" int mesw_rmsnorm(const uint16_t* d_x, int ldx, const uint16_t* d_w, int B, int H, float eps,
-                            uint16_t* d_y, int ldy, void* stream) {
-  if (B <= 0 || H % 2) return mesw_fail(MESW_ERR_VALUE, "rmsnorm: bad shape");
-  rmsnorm_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(d_x, ldx, d_w, H, eps, d_y, ldy);
+                            uint16_t* d_y, int ldy, int y_np, void* stream) {
+  if (B <= 0 || H % 8 || H > kNormThreads * kNormMaxVec * 8 || ldx % 8 || ldy % 8)
+    return mesw_fail(MESW_ERR_VALUE, "rmsnorm: H and strides must be multiples of 8, H <= 8192");
+  if (y_np > 0 && (y_np % 16 || y_np < B)) return mesw_fail(MESW_ERR_VALUE, "rmsnorm: canonical rows must be >= B, multiple of 16");
+  rmsnorm_kernel<<<B, kNormThreads, 0, (cudaStream_t)stream>>>(d_x, ldx, d_w, H, eps, d_y, ldy, y_np);
   return mesw_check_launch("rmsnorm");
 }
 
@@ -284,26 +395,28 @@ extern "C" int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_po
 extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
                                      const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
                                      int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
-                                     void* stream) {
-  if (B <= 0 || n_kv <= 0 || n_heads % n_kv || head_dim % 64)
-    return mesw_fail(MESW_ERR_VALUE, "attention: bad shape");
+                                     int out_np, void* stream) {
+  if (B <= 0 || n_kv <= 0 || n_heads % n_kv) return mesw_fail(MESW_ERR_VALUE, "attention: bad shape");
+  if (head_dim != 128) return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: head_dim must be 128");
+  if (ctx_max > kAttnMaxCtx) return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: context window > 320");
   const int G = n_heads / n_kv;
-  const size_t smem = (size_t)G * (ctx_max + head_dim) * sizeof(float);
-  if (smem > 200 * 1024) return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: context too long");
+  const size_t smem = (size_t)2 * kAttnMaxCtx * kAttnRow * 2 +
+                      ((size_t)G * 128 + (size_t)kAttnMaxCtx * G + (size_t)8 * G * 128) * sizeof(float);
   const float scale = 1.0f / sqrtf((float)head_dim);
   dim3 grid(B, n_kv);
   cudaStream_t s = (cudaStream_t)stream;
-#define MESW_ATTN(GG)                                                                                  \
-  case GG: {                                                                                           \
-    static bool cfg = false;                                                                           \
-    if (!cfg) {                                                                                        \
-      cudaFuncSetAttribute(attn_decode_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                           200 * 1024);                                                                \
-      cfg = true;                                                                                      \
-    }                                                                                                  \
-    attn_decode_kernel<GG><<<grid, 128, smem, s>>>(d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, head_dim, \
-                                                   ctx_max, scale, d_out, ld_out);                     \
-    break;                                                                                             \
+#define MESW_ATTN(GG)                                                                                   \
+  case GG: {                                                                                            \
+    static bool cfg = false;                                                                            \
+    if (!cfg) {                                                                                         \
+      cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<GG>,                                      \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+      if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));                     \
+      cfg = true;                                                                                       \
+    }                                                                                                   \
+    attn_decode_kernel<GG><<<grid, kAttnThreads, smem, s>>>(d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, \
+                                                            ctx_max, scale, d_out, ld_out, out_np);     \
+    break;                                                                                              \
   }
   switch (G) {
     MESW_ATTN(1)
@@ -318,10 +431,10 @@ extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16
 }
 
 extern "C" int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,
-                           void* stream) {
+                           int out_np, void* stream) {
   if (B <= 0 || I % 2) return mesw_fail(MESW_ERR_VALUE, "swiglu: bad shape");
   dim3 grid((I / 2 + 255) / 256 < 64 ? (I / 2 + 255) / 256 : 64, B);
-  swiglu_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_gu, ld_gu, I, d_out, ld_out);
+  swiglu_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_gu, ld_gu, I, d_out, ld_out, out_np);
   return mesw_check_launch("swiglu");
 }
 
@@ -330,4 +443,20 @@ extern "C" int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int 
   if (B <= 0 || V <= 0) return mesw_fail(MESW_ERR_VALUE, "argmax: bad shape");
   argmax_kernel<<<B, 1024, 0, (cudaStream_t)stream>>>(d_logits, is_bf16, V, ld, d_out);
   return mesw_check_launch("argmax");
+}
+
+extern "C" int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t* d_xc, void* stream) {
+  if (B <= 0 || m <= 0 || ldx < m) return mesw_fail(MESW_ERR_VALUE, "pack_x: bad shape");
+  const int NP = (B + 15) & ~15, n_ks = (m + 127) / 128;
+  const long long total = (long long)n_ks * NP * 16;
+  pack_x_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_x, B, m, ldx, d_xc, NP, n_ks);
+  return mesw_check_launch("pack_x");
+}
+
+extern "C" int mesw_unpack_x(const uint16_t* d_xc, int B, int m, uint16_t* d_y, int ldy, void* stream) {
+  if (B <= 0 || m <= 0 || ldy < m) return mesw_fail(MESW_ERR_VALUE, "unpack_x: bad shape");
+  const int NP = (B + 15) & ~15;
+  const long long total = (long long)B * m;
+  unpack_x_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_xc, B, m, NP, d_y, ldy);
+  return mesw_check_launch("unpack_x");
 }

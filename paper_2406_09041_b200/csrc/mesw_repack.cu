@@ -7,6 +7,7 @@
 
 #include "mesw_common.cuh"
 #include "mesw_host.h"
+#include "mesw_layout.cuh"
 
 namespace mesw {
 
@@ -34,112 +35,85 @@ __device__ __forceinline__ bool is_salient(const int32_t* idx, uint32_t k, uint3
   return false;
 }
 
-// One thread per 32-bit device code word.
+// One thread per 32-bit device code word (layout: mesw_layout.cuh).
 template <int DB>
 __global__ void repack_codes_kernel(const uint8_t* __restrict__ packed, uint32_t m, uint32_t n,
                                     uint32_t bits, const int32_t* __restrict__ sal, uint32_t k,
                                     uint32_t* __restrict__ dst, uint32_t n_ks, uint32_t cg0,
                                     uint32_t n_cg_blk, uint32_t col_base) {
-  constexpr int WPL = 2 * DB;   // words per lane per k-step
-  constexpr int PW = 16 / DB;   // pairs per word
+  constexpr int PW = 16 / DB;                  // pairs per word
+  constexpr int WPU = kUnitN * kUnitK * DB / 32;  // words per unit
+  constexpr int WPC = 2 * DB;                  // words per (kh, m) chunk
   constexpr int OFF = DB == 2 ? 2 : (DB == 4 ? 8 : 128);
-  const uint64_t total = (uint64_t)n_cg_blk * n_ks * kTilesPerCg * 32 * WPL;
+  const uint64_t total = (uint64_t)n_cg_blk * n_ks * WPU;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= total) return;
-  const int word = tid % WPL;
-  uint64_t r = tid / WPL;
-  const int lane = r % 32; r /= 32;
-  const int tile = r % kTilesPerCg; r /= kTilesPerCg;
-  const uint32_t ks = r % n_ks;
-  const uint32_t cg = cg0 + (uint32_t)(r / n_ks);
+  const int wi = (int)(tid % WPU);
+  const uint64_t ul = tid / WPU;  // unit index within the block's column groups
+  const uint32_t ks = (uint32_t)(ul % n_ks);
+  const uint32_t cg = cg0 + (uint32_t)(ul / n_ks);
+  const int w = wi % WPC, mrow = (wi / WPC) % kUnitN, kh = wi / (WPC * kUnitN);
   const uint32_t bpc = (m * bits + 7) / 8;
+  const int64_t jl = (int64_t)cg * kUnitN + mrow - col_base;
   uint32_t out = 0;
 #pragma unroll
   for (int loc = 0; loc < PW; ++loc) {
-    const int p = word * PW + loc;
-    const int kb = p >> 2, reg = p & 3;
+    const int p = w * PW + loc;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      int row, col;
-      frag_coord(lane, reg, h, row, col);
-      const uint32_t i = ks * kTileK + kb * 16 + col;
-      const int64_t jl = (int64_t)cg * kTileN + tile * 16 + row - col_base;
+      const uint32_t i = ks * kUnitK + kh * 64 + 2 * p + h;
       int d = OFF;  // padding and salient rows decode to q = 0
       if (i < m && jl >= 0 && jl < (int64_t)n && !is_salient(sal, k, i))
         d = read_mesw_code(packed, bpc, i, (uint32_t)jl, bits) + OFF;
       out |= uint32_t(d) << (DB * loc + (h ? 16 : 0));
     }
   }
-  dst[((((uint64_t)cg * n_ks + ks) * kTilesPerCg + tile) * 32 + lane) * WPL + word] = out;
+  dst[((uint64_t)cg * n_ks + ks) * WPU + wi] = out;
 }
 
-// One thread per lane-fragment (8 bf16 = 16 bytes).
+// One thread per 16-byte core-matrix row (8 bf16 along k of one output channel).
 __global__ void repack_weight_kernel(const uint16_t* __restrict__ src, uint32_t m, uint32_t n,
-                                     uint32_t ld, int transposed, uint4* __restrict__ dst,
+                                     uint32_t ld, int transposed, uint8_t* __restrict__ dst,
                                      uint32_t n_ks, uint32_t cg0, uint32_t n_cg_blk,
                                      uint32_t col_base) {
-  const uint64_t total = (uint64_t)n_cg_blk * n_ks * kTilesPerCg * kKbPerKs * 32;
+  const uint64_t total = (uint64_t)n_cg_blk * n_ks * kUnitN * (kUnitK / 8);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= total) return;
-  uint64_t r = tid;
-  const int lane = r % 32; r /= 32;
-  const int kb = r % kKbPerKs; r /= kKbPerKs;
-  const int tile = r % kTilesPerCg; r /= kTilesPerCg;
-  const uint32_t ks = r % n_ks;
-  const uint32_t cg = cg0 + (uint32_t)(r / n_ks);
+  const int kc = (int)(tid % (kUnitK / 8));
+  const int mrow = (int)((tid / (kUnitK / 8)) % kUnitN);
+  const uint64_t ul = tid / (kUnitN * (kUnitK / 8));
+  const uint32_t ks = (uint32_t)(ul % n_ks);
+  const uint32_t cg = cg0 + (uint32_t)(ul / n_ks);
+  const int64_t jl = (int64_t)cg * kUnitN + mrow - col_base;
   uint32_t v[4];
 #pragma unroll
-  for (int reg = 0; reg < 4; ++reg) {
+  for (int q = 0; q < 4; ++q) {
     uint32_t pair = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      int row, col;
-      frag_coord(lane, reg, h, row, col);
-      const uint32_t i = ks * kTileK + kb * 16 + col;
-      const int64_t jl = (int64_t)cg * kTileN + tile * 16 + row - col_base;
+      const uint32_t i = ks * kUnitK + kc * 8 + 2 * q + h;
       uint16_t e = 0;
       if (i < m && jl >= 0 && jl < (int64_t)n)
         e = transposed ? src[(uint64_t)jl * ld + i] : src[(uint64_t)i * ld + jl];
       pair |= uint32_t(e) << (h ? 16 : 0);
     }
-    v[reg] = pair;
+    v[q] = pair;
   }
-  dst[((((uint64_t)cg * n_ks + ks) * kTilesPerCg + tile) * kKbPerKs + kb) * 32 + lane] =
-      make_uint4(v[0], v[1], v[2], v[3]);
-}
-
-// Locate element (i, j_global) inside the fragment layouts.
-struct FragLoc {
-  uint64_t unit;  // cg * n_ks + ks
-  int tile, kb, lane, reg, h;
-};
-
-__device__ __forceinline__ FragLoc locate(uint32_t i, uint32_t jg, uint32_t n_ks) {
-  FragLoc L;
-  const uint32_t cg = jg / kTileN, jj = jg % kTileN;
-  const uint32_t ks = i / kTileK, ii = i % kTileK;
-  L.unit = (uint64_t)cg * n_ks + ks;
-  L.tile = jj / 16;
-  const int row = jj % 16;
-  L.kb = ii / 16;
-  const int col = ii % 16;
-  const int g = row & 7, t = (col & 7) >> 1;
-  L.h = col & 1;
-  L.lane = g * 4 + t;
-  L.reg = (row >> 3) + 2 * (col >> 3);
-  return L;
+  uint8_t* unit = dst + ((uint64_t)cg * n_ks + ks) * kUnitWBytes;
+  *reinterpret_cast<uint4*>(unit + w_byte_in_unit(mrow, kc * 8)) = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
 __device__ __forceinline__ int device_code_at(const uint8_t* codes, int db, uint32_t i, uint32_t jg,
                                               uint32_t n_ks) {
-  const FragLoc L = locate(i, jg, n_ks);
-  const int wpl = 2 * db, pw = 16 / db;
-  const int p = L.kb * 4 + L.reg;
-  const int word = p / pw, loc = p % pw;
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(codes) +
-                      ((L.unit * kTilesPerCg + L.tile) * 32 + L.lane) * wpl + word;
-  const int d = (*w >> (db * loc + (L.h ? 16 : 0))) & ((1 << db) - 1);
-  return d - code_offset(db);
+  const uint32_t cg = jg / kUnitN, mrow = jg % kUnitN;
+  const uint32_t ks = i / kUnitK, kk = i % kUnitK;
+  uint32_t wb;
+  int bit;
+  code_loc(db, (int)mrow, (int)kk, wb, bit);
+  const uint64_t unit = (uint64_t)cg * n_ks + ks;
+  const uint32_t word = *reinterpret_cast<const uint32_t*>(codes + unit * (uint64_t)(kUnitN * kUnitK * db / 8) + wb);
+  const int d = (word >> bit) & ((1 << db) - 1);
+  return d - code_off(db);
 }
 
 __global__ void unpack_codes_kernel(const uint8_t* __restrict__ codes, int db, uint32_t m,
@@ -160,23 +134,23 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ codes, int db,
   if (tid >= (uint64_t)m * n) return;
   const uint32_t i = tid / n, j = tid % n;
   const uint32_t jg = col_base + j;
-  const uint32_t cg = jg / kTileN;
+  const uint32_t cg = jg / kUnitN;
   float v = (float)device_code_at(codes, db, i, jg, n_ks) * steps[jg];
   for (int r = sal_off[cg]; r < sal_off[cg + 1]; ++r)
     if ((uint32_t)sal_idx[r] == i)
-      v = __half2float(__ushort_as_half(sal_rows[(uint64_t)r * kTileN + jg % kTileN]));
+      v = __half2float(__ushort_as_half(sal_rows[(uint64_t)r * kUnitN + jg % kUnitN]));
   out[tid] = v;
 }
 
-__global__ void unpack_weight_kernel(const uint16_t* __restrict__ w, uint32_t m, uint32_t n,
+__global__ void unpack_weight_kernel(const uint8_t* __restrict__ w, uint32_t m, uint32_t n,
                                      uint32_t n_ks, uint32_t col_base, uint16_t* __restrict__ out) {
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (uint64_t)m * n) return;
   const uint32_t i = tid / n, j = tid % n;
-  const FragLoc L = locate(i, col_base + j, n_ks);
-  const uint64_t lane_base =
-      (((L.unit * kTilesPerCg + L.tile) * kKbPerKs + L.kb) * 32 + L.lane) * 8;
-  out[tid] = w[lane_base + L.reg * 2 + L.h];
+  const uint32_t jg = col_base + j;
+  const uint64_t unit = (uint64_t)(jg / kUnitN) * n_ks + i / kUnitK;
+  out[tid] = *reinterpret_cast<const uint16_t*>(w + unit * kUnitWBytes +
+                                                w_byte_in_unit((int)(jg % kUnitN), (int)(i % kUnitK)));
 }
 
 }  // namespace mesw
@@ -203,7 +177,7 @@ extern "C" int mesw_repack_codes(const uint8_t* d_packed, uint32_t m, uint32_t n
   const uint32_t n_ks = m_pad / kTileK;
   const uint32_t cg0 = col_base / kTileN;
   const uint32_t n_cg_blk = (n + kTileN - 1) / kTileN;
-  const uint64_t words = (uint64_t)n_cg_blk * n_ks * kTilesPerCg * 32 * 2 * db;
+  const uint64_t words = (uint64_t)n_cg_blk * n_ks * (kUnitN * kUnitK * db / 32);
   cudaStream_t s = (cudaStream_t)stream;
   uint32_t* dst = reinterpret_cast<uint32_t*>(d_codes);
   if (db == 2)
@@ -227,9 +201,9 @@ extern "C" int mesw_repack_weight(const uint16_t* d_src, uint32_t m, uint32_t n,
   if (m == 0 || n == 0) return MESW_OK;
   const uint32_t n_ks = m_pad / kTileK;
   const uint32_t n_cg_blk = (n + kTileN - 1) / kTileN;
-  const uint64_t frags = (uint64_t)n_cg_blk * n_ks * kTilesPerCg * kKbPerKs * 32;
-  repack_weight_kernel<<<grid_for(frags, 256), 256, 0, (cudaStream_t)stream>>>(
-      d_src, m, n, ld, transposed, reinterpret_cast<uint4*>(d_w), n_ks, col_base / kTileN,
+  const uint64_t rows16 = (uint64_t)n_cg_blk * n_ks * kUnitN * (kUnitK / 8);
+  repack_weight_kernel<<<grid_for(rows16, 256), 256, 0, (cudaStream_t)stream>>>(
+      d_src, m, n, ld, transposed, reinterpret_cast<uint8_t*>(d_w), n_ks, col_base / kTileN,
       n_cg_blk, col_base);
   return mesw_check_launch("repack_weight");
 }
@@ -270,6 +244,6 @@ extern "C" int mesw_unpack_weight_debug(const uint16_t* d_w, uint32_t m, uint32_
     return mesw_fail(MESW_ERR_VALUE, "unpack_weight_debug: bad geometry");
   if (m == 0 || n == 0) return MESW_OK;
   unpack_weight_kernel<<<grid_for((uint64_t)m * n, 256), 256, 0, (cudaStream_t)stream>>>(
-      d_w, m, n, m_pad / kTileK, col_base, d_out);
+      reinterpret_cast<const uint8_t*>(d_w), m, n, m_pad / kTileK, col_base, d_out);
   return mesw_check_launch("unpack_weight_debug");
 }

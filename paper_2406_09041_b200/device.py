@@ -25,6 +25,7 @@ from . import _lib
 from .compress import CompressedDelta
 
 TILE = 128
+MAX_ROWS = 192  # padded token rows per fused-linear launch (TMEM budget)
 
 
 def _ceil(v: int, q: int = TILE) -> int:
@@ -274,7 +275,7 @@ class Workspace:
         idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
         with torch.cuda.device(idx):
             self.sms = L.mesw_device_sm_count()
-        self.nbytes = int(L.mesw_linear_workspace_bytes(64, self.sms))
+        self.nbytes = int(L.mesw_linear_workspace_bytes(MAX_ROWS, self.sms))
         self.ws = torch.empty(self.nbytes, dtype=torch.uint8, device=self.device)
         self.counters = torch.zeros(1 << 14, dtype=torch.int32, device=self.device)
 
@@ -289,37 +290,68 @@ class Workspace:
 
 # --------------------------------------------------------------------------- K2 call
 
+def canonical_rows(B: int) -> int:
+    """Rows of the canonical activation layout: B padded to a multiple of 16."""
+    return (B + 15) // 16 * 16
+
+
+def canonical_numel(B: int, m: int) -> int:
+    return _ceil(m) * canonical_rows(B)
+
+
+def pack_x(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Row-major bf16 [B, m] -> canonical tile layout (include/mesw.h, mesw_pack_x)."""
+    if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_cuda or x.stride(1) != 1:
+        raise ValueError("x must be a row-contiguous 2-D bf16 CUDA tensor")
+    B, m = x.shape
+    if out is None:
+        out = torch.empty(canonical_numel(B, m), dtype=torch.bfloat16, device=x.device)
+    _lib.check(_lib.lib().mesw_pack_x(x.data_ptr(), B, m, x.stride(0), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def unpack_x(xc: torch.Tensor, B: int, m: int, stream=None) -> torch.Tensor:
+    y = torch.empty((B, m), dtype=torch.bfloat16, device=xc.device)
+    _lib.check(_lib.lib().mesw_unpack_x(xc.data_ptr(), B, m, y.data_ptr(), m, _stream(stream)))
+    return y
+
+
 class LinearPlan:
     """Pre-built launch of the fused multi-expert linear (pointers bound once).
 
-    Calling the plan issues one `mesw_me_linear` on the current (or given) stream;
-    this keeps per-launch host cost to one ctypes call and makes the launch
-    capturable in a CUDA graph.
+    `xc` holds the B input rows in the canonical tile layout (pack_x / the decoder
+    glue write it).  Calling the plan issues one `mesw_me_linear` on the current (or
+    given) stream; this keeps per-launch host cost to one ctypes call and makes the
+    launch capturable in a CUDA graph.
     """
 
-    def __init__(self, x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
+    def __init__(self, xc: torch.Tensor, B: int, weight: DeviceWeight | None, table: ExpertTable | None,
                  segments, out: torch.Tensor, residual: torch.Tensor | None = None,
                  geom: LinearGeometry | None = None, num_ctas: int = 0, activation: str | None = None):
         L = _lib.lib()
         if geom is None:
             geom = weight.geom if weight is not None else next(
                 d.geom for d in table.deltas if d is not None)
-        if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_cuda:
-            raise ValueError("x must be a 2-D bf16 CUDA tensor")
-        if x.stride(1) != 1 or out.stride(1) != 1:
-            raise ValueError("x and out must be row-contiguous")
+        if xc.dtype != torch.bfloat16 or not xc.is_cuda or not xc.is_contiguous():
+            raise ValueError("xc must be a contiguous bf16 CUDA tensor (canonical layout)")
+        if xc.numel() < canonical_numel(B, geom.m):
+            raise ValueError("xc too small for the canonical layout of B rows")
+        if out.stride(1) != 1:
+            raise ValueError("out must be row-contiguous")
         if out.dtype not in (torch.bfloat16, torch.float32):
             raise ValueError("output must be bf16 or f32")
         segs = [(int(b), int(e), int(s)) for b, e, s in segments]
+        if any(b % 16 for b, _, _ in segs):
+            raise ValueError("LinearPlan segments must start on 16-row boundaries (see align_segments)")
         if len(segs) > _lib.MAX_SEGMENTS:
             raise NotImplementedError(f"more than {_lib.MAX_SEGMENTS} expert segments in one launch")
         self.geom = geom
-        self.keep = (x, weight, table, out, residual)  # keep buffers alive
-        ws = Workspace.get(x.device)
+        self.keep = (xc, weight, table, out, residual)  # keep buffers alive
+        ws = Workspace.get(xc.device)
         self.ws = ws
         a = _lib.LinearArgs()
-        a.x = x.data_ptr()
-        a.B, a.m, a.n, a.ldx = x.shape[0], geom.m, geom.n, x.stride(0)
+        a.x = xc.data_ptr()
+        a.B, a.m, a.n, a.x_layout = B, geom.m, geom.n, 0
         a.w = _ptr(weight.frag) if weight is not None else None
         a.expert_table = table.dev.data_ptr() if table is not None else None
         a.code_bits = table.code_bits if (table is not None and table.code_bits) else 2
@@ -344,19 +376,73 @@ class LinearPlan:
         _lib.check(self._fn(C.byref(self.args), _stream(stream)))
 
 
+def align_segments(B: int, segments) -> tuple:
+    """Re-layout rows so every expert segment starts at a multiple of 16 rows (the
+    kernel's tcgen05 N granularity).  Returns (rows_pad, new_segments, src) where
+    src[new_row] = old row or -1 for padding rows."""
+    segs = sorted((int(b), int(e), int(s)) for b, e, s in segments)
+    src, new_segs = [], []
+    cur = 0
+    for b, e, sl in segs:
+        if cur < b:  # uncovered (base-only) rows keep their place in order
+            src.extend(range(cur, b))
+        while len(src) % 16:
+            src.append(-1)
+        new_segs.append((len(src), len(src) + (e - b), sl))
+        src.extend(range(b, e))
+        cur = e
+    src.extend(range(cur, B))
+    return len(src), new_segs, src
+
+
 def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
               segments, out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
               out_dtype=torch.bfloat16, geom: LinearGeometry | None = None, num_ctas: int = 0,
               activation: str | None = None, stream=None) -> torch.Tensor:
-    """y = x.W + x.Dtilde_{expert(t)} (+ residual) in one fused kernel launch.
+    """y = x.W + x.Dtilde_{expert(t)} (+ residual) -- the fused kernel on row-major inputs.
 
-    x: bf16 [B, ldx] on the GPU with ldx >= m_pad (pad columns zero), rows grouped
-    by expert.  segments: iterable of (begin, end, slot) into `table`.
+    x: bf16 [B, >= m] on the GPU, rows grouped by expert; segments: iterable of
+    (begin, end, slot) into `table`.  The rows are packed into the canonical layout;
+    segments not starting on a 16-row boundary are re-laid out (rows are independent,
+    so results equal those of the caller's layout) and batches beyond the per-launch
+    row budget are split.
     """
     if geom is None:
         geom = weight.geom if weight is not None else next(
             d.geom for d in table.deltas if d is not None)
+    B = x.shape[0]
     if out is None:
-        out = torch.empty((x.shape[0], geom.n), dtype=out_dtype, device=x.device)
-    LinearPlan(x, weight, table, segments, out, residual, geom, num_ctas, activation)(stream)
+        out = torch.empty((B, geom.n), dtype=out_dtype, device=x.device)
+    segs = [(int(b), int(e), int(s)) for b, e, s in segments]
+    xm = x[:, :geom.m] if x.shape[1] >= geom.m else x
+    if all(b % 16 == 0 for b, _, _ in segs) and B <= MAX_ROWS:
+        xc = pack_x(xm.contiguous() if xm.stride(1) != 1 else xm, stream=stream)
+        LinearPlan(xc, B, weight, table, segs, out, residual, geom, num_ctas, activation)(stream)
+        return out
+    rows, new_segs, src = align_segments(B, segs)
+    cuts, start = [], 0
+    while start < rows:
+        end = min(rows, start + MAX_ROWS)
+        cuts.append((start, end))
+        start = end
+    src_all = torch.as_tensor(src, dtype=torch.int64, device=x.device)
+    for c0, c1 in cuts:
+        src_t = src_all[c0:c1]
+        valid = src_t >= 0
+        n_rows = c1 - c0
+        csegs = [(max(b, c0) - c0, min(e, c1) - c0, sl) for b, e, sl in new_segs if b < c1 and e > c0]
+        xp = torch.zeros((n_rows, geom.m), dtype=x.dtype, device=x.device)
+        xp[valid] = xm[src_t[valid]]
+        rp = None
+        if residual is not None:
+            rp = torch.zeros((n_rows, residual.shape[1]), dtype=residual.dtype, device=x.device)
+            rp[valid] = residual[src_t[valid]]
+        yp = torch.empty((n_rows, out.shape[1]), dtype=out.dtype, device=x.device)
+        if weight is None and not csegs:
+            yp.zero_()
+        else:
+            xc = pack_x(xp, stream=stream)
+            LinearPlan(xc, n_rows, weight, table if csegs else None, csegs, yp, rp, geom, num_ctas,
+                       activation)(stream)
+        out[src_t[valid]] = yp[valid]
     return out

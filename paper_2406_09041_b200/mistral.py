@@ -20,7 +20,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan, _stream
+from .device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan, _stream,
+                     canonical_numel, canonical_rows)
 from .synth import MistralShape
 
 PROJ_ORDER = ("q", "k", "v", "o", "gate", "up", "down")
@@ -39,7 +40,7 @@ class LayerWeights:
 class MistralMultiExpert:
     """Base model + resident experts + decode buffers for up to `max_batch` requests."""
 
-    def __init__(self, shape: MistralShape = MistralShape(), max_batch: int = 32, ctx_max: int = 256,
+    def __init__(self, shape: MistralShape = MistralShape(), max_batch: int = 64, ctx_max: int = 256,
                  device="cuda", n_layers: int | None = None):
         self.shape = shape
         self.n_layers = shape.n_layers if n_layers is None else n_layers
@@ -71,11 +72,12 @@ class MistralMultiExpert:
         self.pos = torch.zeros(B, dtype=torch.int32, device=dev)
         self.len = torch.ones(B, dtype=torch.int32, device=dev)
         self.h = torch.zeros((B, s.hidden), dtype=bf, device=dev)
-        self.xn = torch.zeros((B, max(s.hidden, self.g_o.m_pad)), dtype=bf, device=dev)
+        # inputs of the fused linears live in the canonical tile layout (include/mesw.h)
+        self.xn = torch.zeros(canonical_numel(B, s.hidden), dtype=bf, device=dev)
         self.qkv = torch.zeros((B, self.g_qkv.n_pad), dtype=bf, device=dev)
-        self.attn = torch.zeros((B, self.g_o.m_pad), dtype=bf, device=dev)
+        self.attn = torch.zeros(canonical_numel(B, self.g_o.m), dtype=bf, device=dev)
         self.gu = torch.zeros((B, self.g_gu.n_pad), dtype=bf, device=dev)
-        self.act = torch.zeros((B, self.g_down.m_pad), dtype=bf, device=dev)
+        self.act = torch.zeros(canonical_numel(B, self.g_down.m), dtype=bf, device=dev)
         self.logits = torch.zeros((B, self.g_head.n_pad), dtype=bf, device=dev)
         kv_shape = (self.n_layers, B, self.ctx_max, s.n_kv_heads, s.head_dim)
         self.kcache = torch.zeros(kv_shape, dtype=bf, device=dev)
@@ -170,12 +172,14 @@ class MistralMultiExpert:
 
     # ------------------------------------------------------------------ batch
     def set_batch(self, expert_ids: list, prompt_lens: list | None = None) -> np.ndarray:
-        """Fix the request batch.  Requests are regrouped by expert; returns the order
-        (order[i] = caller's request index at engine row i).  Positions start at
-        prompt_lens (the KV cache rows below are assumed filled)."""
-        B = len(expert_ids)
-        if not 1 <= B <= self.max_batch:
-            raise ValueError(f"batch size must be in [1, {self.max_batch}]")
+        """Fix the request batch.  Requests are regrouped by expert and every expert group
+        starts on a 16-row boundary (the fused kernel's tcgen05 N granularity); padding
+        rows are inert.  Returns `rows`: rows[r] = caller's request index at engine row r
+        (-1 for padding).  Positions start at prompt_lens (cache rows below are assumed
+        filled)."""
+        n = len(expert_ids)
+        if n < 1:
+            raise ValueError("empty batch")
         slots = []
         for e in expert_ids:
             if e is None:
@@ -186,25 +190,33 @@ class MistralMultiExpert:
             else:
                 slots.append(self.experts[e][0])
         slots = np.asarray(slots)
-        order = np.argsort(slots, kind="stable")
-        segs, cur = [], 0
-        for sl in sorted(set(slots.tolist())):
-            cnt = int((slots == sl).sum())
-            if sl >= 0:
-                segs.append((cur, cur + cnt, int(sl)))
-            cur += cnt
-        pl = np.zeros(B, np.int64) if prompt_lens is None else np.asarray(prompt_lens, np.int64)[order]
-        if (pl >= self.ctx_max).any():
+        rows, segs = [], []
+        for sl in sorted(set(slots.tolist()) - {-1}):
+            while len(rows) % 16:
+                rows.append(-1)
+            members = np.flatnonzero(slots == sl).tolist()
+            segs.append((len(rows), len(rows) + len(members), int(sl)))
+            rows.extend(members)
+        rows.extend(np.flatnonzero(slots == -1).tolist())  # base-only requests
+        B = len(rows)
+        if B > self.max_batch:
+            raise ValueError(f"padded batch of {B} rows exceeds max_batch={self.max_batch}")
+        rows = np.asarray(rows)
+        pl_req = np.zeros(n, np.int64) if prompt_lens is None else np.asarray(prompt_lens, np.int64)
+        if (pl_req >= self.ctx_max).any():
             raise ValueError("prompt longer than the cache window")
+        pl = np.where(rows >= 0, pl_req[np.maximum(rows, 0)], 0)
         if getattr(self, "B", None) != B or getattr(self, "segments", None) != segs:
             self._plans = None  # launch geometry changed: rebuild plans / re-capture
             self.graph = None
         self.B = B
-        self.order = order
+        self.n_requests = n
+        self.rows = rows
+        self.order = rows
         self.segments = segs
         self.pos[:B] = torch.as_tensor(pl, dtype=torch.int32)
         self.len[:B] = torch.as_tensor(pl + 1, dtype=torch.int32)
-        return order
+        return rows
 
     def fill_random_kv(self, prompt_len: int, seed: int = 1) -> None:
         """Synthetic prompt state: random K/V for positions < prompt_len (bench only)."""
@@ -221,12 +233,12 @@ class MistralMultiExpert:
         for l, lw in enumerate(self.layers):
             tq, to, tgu, td = self.tables[l]
             plans.append((
-                LinearPlan(self.xn[:B, :self.g_qkv.m_pad], lw.qkv, tq if segs else None, segs, self.qkv[:B]),
-                LinearPlan(self.attn[:B], lw.o, to if segs else None, segs, self.h[:B], residual=self.h[:B]),
-                LinearPlan(self.xn[:B, :self.g_gu.m_pad], lw.gateup, tgu if segs else None, segs, self.gu[:B]),
-                LinearPlan(self.act[:B], lw.down, td if segs else None, segs, self.h[:B], residual=self.h[:B]),
+                LinearPlan(self.xn, B, lw.qkv, tq if segs else None, segs, self.qkv[:B]),
+                LinearPlan(self.attn, B, lw.o, to if segs else None, segs, self.h[:B], residual=self.h[:B]),
+                LinearPlan(self.xn, B, lw.gateup, tgu if segs else None, segs, self.gu[:B]),
+                LinearPlan(self.act, B, lw.down, td if segs else None, segs, self.h[:B], residual=self.h[:B]),
             ))
-        head = LinearPlan(self.xn[:B, :self.g_head.m_pad], self.head, None, [], self.logits[:B])
+        head = LinearPlan(self.xn, B, self.head, None, [], self.logits[:B])
         self._plans = (plans, head)
 
     def step(self, stream=None) -> None:
@@ -239,12 +251,13 @@ class MistralMultiExpert:
         chk = _lib.check
         plans, head = self._plans
         H = s.hidden
+        NP = canonical_rows(B)
         chk(L.mesw_embed(self.ids.data_ptr(), B, self.embedding.data_ptr(), H, self.h.data_ptr(),
                          self.h.stride(0), st))
         for l, lw in enumerate(self.layers):
             p_qkv, p_o, p_gu, p_down = plans[l]
             chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), lw.attn_norm.data_ptr(), B, H,
-                               C.c_float(s.rms_eps), self.xn.data_ptr(), self.xn.stride(0), st))
+                               C.c_float(s.rms_eps), self.xn.data_ptr(), 0, NP, st))
             p_qkv(stream)
             kc, vc = self.kcache[l], self.vcache[l]
             chk(L.mesw_rope_append(self.qkv.data_ptr(), self.qkv.stride(0), self.pos.data_ptr(), B, s.n_heads,
@@ -252,16 +265,16 @@ class MistralMultiExpert:
                                    vc.data_ptr(), self.ctx_max, st))
             chk(L.mesw_attention_decode(self.qkv.data_ptr(), self.qkv.stride(0), kc.data_ptr(), vc.data_ptr(),
                                         self.len.data_ptr(), B, s.n_heads, s.n_kv_heads, s.head_dim,
-                                        self.ctx_max, self.attn.data_ptr(), self.attn.stride(0), st))
+                                        self.ctx_max, self.attn.data_ptr(), 0, NP, st))
             p_o(stream)
             chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), lw.mlp_norm.data_ptr(), B, H,
-                               C.c_float(s.rms_eps), self.xn.data_ptr(), self.xn.stride(0), st))
+                               C.c_float(s.rms_eps), self.xn.data_ptr(), 0, NP, st))
             p_gu(stream)
             chk(L.mesw_swiglu(self.gu.data_ptr(), self.gu.stride(0), B, s.intermediate, self.act.data_ptr(),
-                              self.act.stride(0), st))
+                              0, NP, st))
             p_down(stream)
         chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), self.final_norm.data_ptr(), B, H,
-                           C.c_float(s.rms_eps), self.xn.data_ptr(), self.xn.stride(0), st))
+                           C.c_float(s.rms_eps), self.xn.data_ptr(), 0, NP, st))
         head(stream)
         chk(L.mesw_argmax(self.logits.data_ptr(), 1, B, s.vocab, self.logits.stride(0), self.ids.data_ptr(), st))
         chk(L.mesw_advance_positions(self.pos.data_ptr(), self.len.data_ptr(), B, self.ctx_max,

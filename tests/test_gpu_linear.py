@@ -234,3 +234,18 @@ def test_c1_shape_mixed_decode():
     y = me_linear(x, dw, table, segs, out_dtype=torch.float32).cpu().numpy()
     ref = _oracle_linear(x.float().cpu().numpy(), w_bf, experts, segs, geom, 8)
     assert _rel(y, ref) <= 2e-3
+
+
+def test_pack_x_roundtrip_and_layout():
+    torch = _torch()
+    from paper_2406_09041_b200.device import canonical_rows, pack_x, unpack_x
+    g = torch.Generator().manual_seed(3)
+    for B, m in [(1, 5), (7, 200), (16, 128), (37, 300)]:
+        x = torch.randn(B, m, generator=g).to(torch.bfloat16).cuda()
+        xc = pack_x(x)
+        assert torch.equal(unpack_x(xc, B, m), x)
+        NP = canonical_rows(B)
+        flat = xc.cpu()
+        t, k = B - 1, m - 1
+        idx = (k // 128) * NP * 128 + (t // 8) * 1024 + ((k % 128) // 8) * 64 + (t % 8) * 8 + k % 8
+        assert flat[idx] == x[t, k].cpu()

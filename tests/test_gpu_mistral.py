@@ -17,7 +17,7 @@ def _bf(a):
 
 def _mini():
     from paper_2406_09041_b200.synth import MistralShape
-    return MistralShape(hidden=256, intermediate=384, n_layers=2, n_heads=4, n_kv_heads=2, head_dim=64,
+    return MistralShape(hidden=256, intermediate=384, n_layers=2, n_heads=2, n_kv_heads=1, head_dim=128,
                         vocab=1000, rope_theta=10000.0)
 
 
@@ -39,7 +39,7 @@ def _build(shape, n_experts=3, seed=0, B=5):
         lw["attn_norm"] = _bf(1 + 0.1 * rng.normal(size=s.hidden))
         lw["mlp_norm"] = _bf(1 + 0.1 * rng.normal(size=s.hidden))
         W["layers"].append(lw)
-    eng = MistralMultiExpert(s, max_batch=8, ctx_max=32)
+    eng = MistralMultiExpert(s, max_batch=64, ctx_max=32)
     eng.load_base(torch.from_numpy(W["embedding"]), torch.from_numpy(W["final_norm"]),
                   torch.from_numpy(W["head"]),
                   [{k: torch.from_numpy(v) for k, v in lw.items()} for lw in W["layers"]])
@@ -66,30 +66,36 @@ def test_decode_step_matches_oracle():
     eng, W, dense = _build(shape)
     B, prompt = 5, 6
     experts = ["e1", "e0", "e2", "e1", None]
-    order = eng.set_batch(experts, [prompt] * B)
+    rows = eng.set_batch(experts, [prompt] * B)
+    R = eng.B
+    real = np.flatnonzero(rows >= 0)  # engine rows holding requests
+    assert sorted(rows[real].tolist()) == list(range(B))
+    for b, e, sl in eng.segments:  # expert groups start on 16-row boundaries
+        assert b % 16 == 0
     rng = np.random.default_rng(3)
     kc = _bf(rng.normal(0, 0.5, size=eng.kcache.shape))
     vc = _bf(rng.normal(0, 0.5, size=eng.vcache.shape))
     eng.kcache.copy_(torch.from_numpy(kc).to(torch.bfloat16))
     eng.vcache.copy_(torch.from_numpy(vc).to(torch.bfloat16))
     ids = rng.integers(0, shape.vocab, size=B)
-    eng.ids[:B] = torch.from_numpy(ids[order].astype(np.int32)).cuda()
+    row_ids = np.where(rows >= 0, ids[np.maximum(rows, 0)], 0).astype(np.int32)
+    eng.ids[:R] = torch.from_numpy(row_ids).cuda()
     eng.step()
     torch.cuda.synchronize()
-    logits = eng.logits[:B, :shape.vocab].float().cpu().numpy()
-    nxt = eng.ids[:B].cpu().numpy()
+    logits = eng.logits[:R, :shape.vocab].float().cpu().numpy()[real]
+    nxt = eng.ids[:R].cpu().numpy()[real]
     slot = {f"e{i}": i for i in range(3)}
-    exp_of = [slot[experts[i]] if experts[i] is not None else -1 for i in order]
-    kco = [[kc[l][b].astype(np.float64).copy() for b in range(B)] for l in range(shape.n_layers)]
-    vco = [[vc[l][b].astype(np.float64).copy() for b in range(B)] for l in range(shape.n_layers)]
-    ref, ref_ids = omis.decode_step(shape, W, dense, kco, vco, ids[order], [prompt] * B, exp_of)
+    exp_of = [slot[experts[rows[r]]] if experts[rows[r]] is not None else -1 for r in real]
+    kco = [[kc[l][r].astype(np.float64).copy() for r in real] for l in range(shape.n_layers)]
+    vco = [[vc[l][r].astype(np.float64).copy() for r in real] for l in range(shape.n_layers)]
+    ref, ref_ids = omis.decode_step(shape, W, dense, kco, vco, row_ids[real], [prompt] * len(real), exp_of)
     err = np.max(np.abs(logits - ref)) / np.max(np.abs(ref))
     assert err <= 2e-2, err  # bf16 activations between kernels; f32 accumulation
     agree = float(np.mean(nxt == ref_ids))
     assert agree >= 0.8, agree
     # positions advanced, cache row written
-    assert eng.pos[:B].cpu().tolist() == [prompt + 1] * B
-    k_new = eng.kcache[0, :B, prompt].float().cpu().numpy()
+    assert eng.pos[:R].cpu().numpy()[real].tolist() == [prompt + 1] * len(real)
+    k_new = eng.kcache[0, :R, prompt].float().cpu().numpy()[real]
     assert np.max(np.abs(k_new - np.stack(kco[0])[:, prompt])) <= 3e-2 * np.max(np.abs(k_new))
 
 
@@ -100,6 +106,7 @@ def test_graph_replay_matches_eager():
     B = 6
     eng.set_batch(["e0", "e1", "e2", "e0", "e1", "e2"], [4] * B)
     eng.fill_random_kv(4)
+    B = eng.B  # engine rows incl. padding
     start_ids = torch.arange(B, dtype=torch.int32, device="cuda") * 7
     eng.ids[:B] = start_ids
     eng.step()

@@ -1,0 +1,33 @@
+"""Per-CTA phase timing of one fused-linear launch (MESW_TIMING=1)."""
+import ctypes as C, os, sys
+os.environ["MESW_TIMING"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2406_09041_b200 import _lib
+from paper_2406_09041_b200.device import LinearPlan, pack_x
+from kbench import make
+L = _lib.lib()
+L.mesw_debug_timing_copy.argtypes = [C.c_void_p, C.c_int]
+m, n = int(sys.argv[1]), int(sys.argv[2])
+E, rows = int(sys.argv[3]), int(sys.argv[4])
+geom, dw, table = make(m, n, max(E, 1), 0)
+segs = [(16 * i, 16 * i + 3, i) for i in range(E)] if E else []
+rows = max(rows, 16 * (E - 1) + 3) if E else rows
+x = torch.randn((rows, m), device="cuda").to(torch.bfloat16)
+y = torch.empty((rows, n), dtype=torch.bfloat16, device="cuda")
+plan = LinearPlan(pack_x(x), rows, dw, table if E else None, segs, y, geom=geom)
+for _ in range(3): plan()
+torch.cuda.synchronize()
+plan(); torch.cuda.synchronize()
+G = min(148, (n // 128) * (m // 128))
+buf = np.zeros(G * 8, np.uint64)
+_lib.check(L.mesw_debug_timing_copy(buf.ctypes.data, G))
+t = buf.reshape(G, 8).astype(np.int64)
+t0 = t[:, 0].min()
+names = ["start", "prod_done", "mma_unit0", "mma_done", "epi_piece0", "epi_last", "cta_end"]
+print(f"m={m} n={n} E={E} rows={rows}  (us from first CTA start)")
+for i, nm in enumerate(names):
+    v = (t[:, i] - t0) / 1e3
+    v = v[t[:, i] > 0]
+    if v.size:
+        print(f"  {nm:12s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f}")

@@ -1,0 +1,79 @@
+// Microbenchmark: tcgen05.mma issue rate on B200 (sm_100a).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t a) {
+  return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)8 << 16) | ((uint64_t)128 << 32) | (1ull << 46);
+}
+__device__ __forceinline__ uint32_t idesc(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__global__ void bench(int M, int N, int R, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tb)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3F803F80u;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t t = tb;
+  if (warp == 1) {
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 65536);
+    const uint32_t id = idesc(M, N);
+    const uint64_t da = sdesc(a), db = sdesc(b);
+    unsigned long long g0, g1;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g0));
+    long long c0 = clock64();
+    if (threadIdx.x == 32) {
+      for (int i = 0; i < R; i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mma_ss(t, da + 16 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    }
+    __syncwarp();
+    long long c1 = clock64();
+    asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra W;\n}\n" ::"r"(smem_u32(&bar)));
+    long long c2 = clock64();
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g1));
+    if (threadIdx.x == 32) { out[0] = c1 - c0; out[1] = c2 - c0; out[2] = g1 - g0; }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 32);
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+  const int R = 4096;
+  for (int rep = 0; rep < 2; ++rep)
+    for (int M : {64, 128})
+      for (int N : {16, 64, 128, 256}) {
+        bench<<<1, 128, 131072>>>(M, N, R, d);
+        unsigned long long h[3];
+        cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+        double macs = (double)M * N * 16;
+        printf("M=%3d N=%3d: issue %6.1f cyc/mma, complete %6.1f cyc/mma, %6.1f ns/mma, %7.0f MAC/cyc, clk %.2f GHz\n",
+               M, N, (double)h[0] / R, (double)h[1] / R, (double)h[2] / R, macs / ((double)h[1] / R),
+               (double)h[1] / h[2]);
+      }
+  printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  return 0;
+}
