@@ -151,7 +151,8 @@ typedef struct {
 
 typedef struct {
   const uint16_t* x;  /* bf16 activations, canonical tile layout (mesw_pack_x)  */
-  int32_t B, m, n;
+  int32_t B, m, n;   /* n: output columns written; device buffers must cover
+                         ceil(n/256)*256 columns (column groups come in pairs) */
   int32_t x_layout;   /* must be 0 (canonical)                                 */
   const uint16_t* w;  /* fragment-layout bf16 base, or NULL (delta only)      */
   const mesw_expert_dev* expert_table; /* DEVICE array indexed by slot        */
@@ -173,10 +174,12 @@ typedef struct {
 } mesw_linear_args;
 
 /* Canonical activation layout consumed by mesw_me_linear: rows padded to
- * NP = ceil16(B); for each 128-wide k-step ks a tile of NP*128 bf16 laid out as
- * [NP/8 row groups][16 k-chunks][8 rows][8 elems] (the UMMA K-major SWIZZLE_NONE
- * canonical B operand), so one bulk copy stages it:
- *   index(t, k) = (k/128)*NP*128 + (t/8)*1024 + ((k%128)/8)*64 + (t%8)*8 + k%8.
+ * NP = ceil16(B); for each 128-wide k-step ks a tile of NP*128 bf16 split in two
+ * halves h (rows 0-7 / 8-15 of every 16-row window -- the N split of a cta_group::2
+ * MMA between the two CTAs of a pair), each [NP/16 windows][16 k-chunks][8 rows][8]
+ * (the UMMA K-major SWIZZLE_NONE canonical B operand), so one bulk copy per CTA stages it:
+ *   index(t, k) = (k/128)*NP*128 + ((t/8)%2)*(NP/2)*128 + (t/16)*1024
+ *                 + ((k%128)/8)*64 + (t%8)*8 + k%8.
  * Rows >= B and columns >= m are written as 0. */
 int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t* d_xc, void* stream);
 /* Inverse (debug / tests): canonical -> row-major [B][ldy]. */

@@ -15,7 +15,8 @@ namespace mesw {
 
 // Canonical activation layout of mesw.h (consumed by the fused linear).
 __device__ __forceinline__ size_t canon_index(int t, int k, int NP) {
-  return (size_t)(k >> 7) * NP * 128 + (size_t)(t >> 3) * 1024 + ((k & 127) >> 3) * 64 + (t & 7) * 8 + (k & 7);
+  return (size_t)(k >> 7) * NP * 128 + (size_t)((t >> 3) & 1) * (NP / 2) * 128 + (size_t)(t >> 4) * 1024 +
+         ((k & 127) >> 3) * 64 + (t & 7) * 8 + (k & 7);
 }
 
 // Output address of element (t, k): row-major with ld, or canonical when np > 0.

@@ -31,8 +31,11 @@
 namespace mesw {
 
 constexpr int kDqGroups = 2;  // dequant warpgroups: group g expands k-half g of every job
-constexpr int kProducerWarp = 0, kMmaWarp = 1, kDqWarp0 = 2, kEpiWarp0 = 2 + 4 * kDqGroups;
-constexpr int kThreads = (kEpiWarp0 + 4) * 32;  // 14 warps
+// warp roles: 0 weight-tile producer, 1 base-MMA issuer, 2 x-tile producer, 3 code producer,
+// 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
+constexpr int kWProdWarp = 0, kMmaWarp = 1, kXProdWarp = 2, kCProdWarp = 3;
+constexpr int kDqWarp0 = 4, kEpiWarp0 = kDqWarp0 + 4 * kDqGroups;
+constexpr int kThreads = (kEpiWarp0 + 4) * 32;  // 16 warps
 constexpr int kTmemCols = 512;
 constexpr int kMaxASlots = 6;
 constexpr int kAColsPerSlot = 64;
@@ -42,9 +45,12 @@ constexpr int kXRowGroupBytes = 2048;  // 8 token rows x 16 k-chunks x 16 B
 constexpr int kSalFast = 16;           // salient rows per column group handled from smem
 
 // Element index of x[t][k] in the canonical activation layout (see mesw.h): per 128-wide
-// k-step a [NP/8 row groups][16 k-chunks][8 rows][8 elems] tile of NP*128 bf16.
+// k-step, two halves h = (t/8)%2 (rows 0-7 / 8-15 of every 16-row window), each a
+// [NP/16 windows][16 k-chunks][8 rows][8 elems] UMMA K-major tile -- the B-operand split
+// of a cta_group::2 MMA (CTA h of the pair holds half h).
 __device__ __forceinline__ size_t xc_index(int t, int k, int NP) {
-  return (size_t)(k >> 7) * NP * 128 + (size_t)(t >> 3) * 1024 + ((k & 127) >> 3) * 64 + (t & 7) * 8 + (k & 7);
+  return (size_t)(k >> 7) * NP * 128 + (size_t)((t >> 3) & 1) * (NP / 2) * 128 + (size_t)(t >> 4) * 1024 +
+         ((k & 127) >> 3) * 64 + (t & 7) * 8 + (k & 7);
 }
 
 struct SegDesc {
@@ -89,7 +95,7 @@ struct Smem {
   uint64_t xfull[kMaxStages], xempty[kMaxStages];
   uint64_t wfull[kMaxStages], wempty[kMaxStages];
   uint64_t cfull[kMaxStages], cempty[kMaxStages];
-  uint64_t aempty[kMaxASlots];
+  uint64_t afull[kMaxASlots], aempty[kMaxASlots];
   uint64_t accfull[2], accempty[2];
   uint32_t tmem_base;
   int flag;
@@ -112,6 +118,10 @@ __device__ __forceinline__ uint32_t idesc_bf16(int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
+__device__ __forceinline__ uint32_t idesc_bf16_m256(int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -124,6 +134,60 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// cta_group::2 (M = 256 over a CTA pair) variants; only the leader CTA issues.
+__device__ __forceinline__ void mma2_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma2_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// Commit the issuing thread's MMAs to the same-offset mbarrier in both CTAs of the pair.
+__device__ __forceinline__ void tc2_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// mbarrier arrive on the same-offset barrier of CTA `rank` in the cluster (release.cluster).
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// Wait with cluster-scope acquire (barriers that receive arrivals from the peer CTA).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -166,6 +230,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 #undef MESW_R8
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
@@ -227,6 +301,29 @@ __device__ __forceinline__ void dequant_chunk<8>(const uint32_t* cw, uint32_t* r
       r[2 * w + l] = d;
     }
 }
+
+// Order in which a CTA walks its unit range [u0, u1): piece 0 = the run in the LAST
+// column group, piece 1 = the run in the FIRST column group, then the middle column
+// groups in order.  The two boundary pieces are the ones shared with neighbouring CTAs
+// (stream-K), so their cross-CTA reductions happen early and overlap the main loop
+// instead of forming a tail.
+struct PieceOrder {
+  long long u0, u1;
+  int n_ks, cg_lo, cg_hi, np;
+  __device__ __forceinline__ PieceOrder(long long a, long long b, int nks) : u0(a), u1(b), n_ks(nks) {
+    cg_lo = (int)(a / nks);
+    cg_hi = (int)((b - 1) / nks);
+    np = b > a ? cg_hi - cg_lo + 1 : 0;
+  }
+  __device__ __forceinline__ int cg_of(int idx) const {
+    return idx == 0 ? cg_hi : (idx == 1 ? cg_lo : cg_lo + idx - 1);
+  }
+  __device__ __forceinline__ void bounds(int idx, long long& a, long long& b) const {
+    const long long c0 = (long long)cg_of(idx) * n_ks;
+    a = c0 > u0 ? c0 : u0;
+    b = c0 + n_ks < u1 ? c0 + n_ks : u1;
+  }
+};
 
 __device__ __forceinline__ int unit_owner(long long u, long long T, int G) {
   return (int)(((u + 1) * (long long)G - 1) / T);
@@ -351,31 +448,43 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do { if (p.tbuf) p.tbuf[(size_t)blockIdx.x * 8 + (i)] = gtimer(); } while (0)
 
 // ---------------------------------------------------------------- kernel
+// A cluster of two CTAs ("pair") owns two adjacent column groups (256 output channels)
+// and issues cta_group::2 MMAs with M = 256: every tcgen05.mma covers both column groups,
+// halving the tensor-pipe instruction count (the bound at decode batch sizes).  Each CTA
+// streams its own column group's weight tiles and codes, its own half of every 16-row
+// activation window (B is split along N between the pair), dequantises its own A rows into
+// its own TMEM, and drains its own accumulators; the leader (rank 0) issues all MMAs and
+// commits them to both CTAs' barriers (multicast).  The peer relays its "tile landed"
+// events to the leader's barriers.
 template <int DB>
 __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_constant__ LinearParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   Smem& S = *reinterpret_cast<Smem*>(smem);
   uint8_t* ring = smem + ring_offset();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
-  const long long u0 = (long long)c * p.T / p.G, u1 = (long long)(c + 1) * p.T / p.G;
+  const uint32_t rank = cluster_rank();
+  const int c = blockIdx.x;         // CTA index (stream-K slots)
+  const int c2 = blockIdx.x >> 1;   // pair index
+  const long long T2 = p.T, G2 = p.G / 2;
+  const long long u0 = (long long)c2 * T2 / G2, u1 = (long long)(c2 + 1) * T2 / G2;  // pair units
+  const PieceOrder po(u0, u1, p.n_ks);
   constexpr int CB = kUnitN * kUnitK * DB / 8;  // code bytes per unit per expert
   constexpr int CHB = 8 * DB;                   // code bytes per (k-half, channel)
-  const int NP = p.NP;
+  const int NP = p.NP, HP = NP / 2;             // rows per launch / per CTA half
 
-  const int n_issuers = 1 + (p.n_seg > 0 ? kDqGroups : 0);  // MMA warp + dequant groups
   if (threadIdx.x == 0) {
-    for (int i = 0; i < p.nx; ++i) { mbar_init(&S.xfull[i], 1); mbar_init(&S.xempty[i], n_issuers); }
-    for (int i = 0; i < p.nw; ++i) { mbar_init(&S.wfull[i], 1); mbar_init(&S.wempty[i], 1); }
+    const uint32_t peer_relay = rank == 0 ? 2 : 1;  // leader: own tile + peer relay
+    for (int i = 0; i < p.nx; ++i) { mbar_init(&S.xfull[i], peer_relay); mbar_init(&S.xempty[i], 1); }
+    for (int i = 0; i < p.nw; ++i) { mbar_init(&S.wfull[i], peer_relay); mbar_init(&S.wempty[i], 1); }
     for (int i = 0; i < p.nc; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 128 * kDqGroups); }
-    for (int i = 0; i < p.n_aslots; ++i) mbar_init(&S.aempty[i], 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], n_issuers); mbar_init(&S.accempty[i], 4); }
+    for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 8); mbar_init(&S.aempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], 1); mbar_init(&S.accempty[i], 8); }
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
                  "n"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   for (int i = threadIdx.x; i < kMaxRows; i += kThreads) S.tok2seg[i] = -1;
   __syncthreads();
@@ -396,269 +505,281 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
   tc_fence_after();
   const uint32_t tbase = S.tmem_base;
   const bool has_w = p.w != nullptr;
   if (threadIdx.x == 0) MESW_STAMP(0);
 
-  if (warp == kProducerWarp) {
-    // ===================== producer: x tiles, weight tiles, code chunks =====================
-    int sx = 0, sw = 0, sc = 0;
-    uint32_t px = 0, pw = 0, pc = 0;
-    bool fx = true, fw = true, fc = true;
-    int ks = (int)(u0 % p.n_ks);
-    for (long long u = u0; u < u1; ++u) {
-      if (lane == 0) {
-        if (!fx) mbar_wait(&S.xempty[sx], px ^ 1);
-        mbar_arrive_expect_tx(&S.xfull[sx], (uint32_t)p.xbytes);
-        bulk_g2s(ring + p.xo + (size_t)sx * p.xbytes, p.x + (size_t)ks * NP * kUnitK, p.xbytes, &S.xfull[sx]);
-        if (++sx == p.nx) { sx = 0; px ^= 1; fx = false; }
-        if (has_w) {
-          if (!fw) mbar_wait(&S.wempty[sw], pw ^ 1);
-          mbar_arrive_expect_tx(&S.wfull[sw], kUnitWBytes);
-          bulk_g2s(ring + p.wo + (size_t)sw * kUnitWBytes, p.w + (size_t)u * kUnitWBytes, kUnitWBytes, &S.wfull[sw]);
-          if (++sw == p.nw) { sw = 0; pw ^= 1; fw = false; }
+  if (warp == kWProdWarp || warp == kXProdWarp || warp == kCProdWarp) {
+    // ===================== producers (own column group / own x half) =====================
+    uint64_t evict_first;  // weights / codes are streamed once: do not let them evict partials
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
+    int st = 0;
+    uint32_t ph = 0;
+    bool first = true;
+    for (int pi = 0; pi < po.np; ++pi) {
+      long long pa, pb;
+      po.bounds(pi, pa, pb);
+      const int cgp = po.cg_of(pi);
+      const int cg = 2 * cgp + (int)rank;
+      for (long long u = pa; u < pb; ++u) {
+        const int ks = (int)(u - (long long)cgp * p.n_ks);
+        const long long unit = (long long)cg * p.n_ks + ks;  // this CTA's unit
+        if (warp == kXProdWarp) {
+          if (lane == 0) {
+            if (!first) mbar_wait(&S.xempty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&S.xfull[st], (uint32_t)p.xbytes);
+            bulk_g2s(ring + p.xo + (size_t)st * p.xbytes, p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK,
+                     p.xbytes, &S.xfull[st]);
+            if (++st == p.nx) { st = 0; ph ^= 1; first = false; }
+          }
+        } else if (warp == kWProdWarp) {
+          if (lane == 0 && has_w) {
+            if (!first) mbar_wait(&S.wempty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&S.wfull[st], kUnitWBytes);
+            bulk_g2s_hint(ring + p.wo + (size_t)st * kUnitWBytes, p.w + (size_t)unit * kUnitWBytes, kUnitWBytes,
+                          &S.wfull[st], evict_first);
+            if (++st == p.nw) { st = 0; ph ^= 1; first = false; }
+          }
+        } else {
+          for (int ch = 0; ch < p.n_chunks; ++ch) {
+            const int sg0 = ch * p.segs_per_chunk;
+            const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
+            if (lane == 0) {
+              if (!first) mbar_wait(&S.cempty[st], ph ^ 1);
+              mbar_arrive_expect_tx(&S.cfull[st], (uint32_t)(sg1 - sg0) * CB);
+            }
+            __syncwarp();
+            for (int q = sg0 + lane; q < sg1; q += 32)
+              bulk_g2s_hint(ring + p.co + (size_t)st * p.cbytes + (size_t)(q - sg0) * CB,
+                            S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[st], evict_first);
+            __syncwarp();
+            if (++st == p.nc) { st = 0; ph ^= 1; first = false; }
+          }
         }
       }
-      for (int ch = 0; ch < p.n_chunks; ++ch) {
-        const int sg0 = ch * p.segs_per_chunk;
-        const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-        if (lane == 0) {
-          if (!fc) mbar_wait(&S.cempty[sc], pc ^ 1);
-          mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
-        }
-        __syncwarp();
-        for (int q = sg0 + lane; q < sg1; q += 32)
-          bulk_g2s(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB, S.segs[q].codes + (size_t)u * CB,
-                   CB, &S.cfull[sc]);
-        __syncwarp();
-        if (++sc == p.nc) { sc = 0; pc ^= 1; fc = false; }
-      }
-      if (++ks == p.n_ks) ks = 0;
     }
-    if (lane == 0) MESW_STAMP(1);
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (one thread) =====================
-    // The tensor pipe accepts one tcgen05.mma per ~45 cycles at these shapes, so the
-    // issue loop is kept minimal: all smem descriptors are precomputed and advanced by
-    // plain 64-bit adds (start address field += bytes/16), the k-loop is unrolled.
-    if (lane == 0) {
+    if (rank != 0) {
+      // ===================== peer: relay "x / weight tile landed" to the leader =====================
+      if (lane == 0) {
+        int sx = 0, sw = 0;
+        uint32_t px = 0, pw = 0;
+        for (int pi = 0; pi < po.np; ++pi) {
+          long long pa, pb;
+          po.bounds(pi, pa, pb);
+          for (long long u = pa; u < pb; ++u) {
+            mbar_wait(&S.xfull[sx], px);
+            mbar_arrive_cta(&S.xfull[sx], 0);
+            if (++sx == p.nx) { sx = 0; px ^= 1; }
+            if (has_w) {
+              mbar_wait(&S.wfull[sw], pw);
+              mbar_arrive_cta(&S.wfull[sw], 0);
+              if (++sw == p.nw) { sw = 0; pw ^= 1; }
+            }
+          }
+        }
+      }
+    } else if (lane == 0) {
+      // ===================== leader: issue every MMA of the pair =====================
       const uint64_t xdesc0 = smem_desc(smem_u32(ring + p.xo));
       const uint64_t wdesc0 = smem_desc(smem_u32(ring + p.wo));
       const uint32_t xstride = (uint32_t)p.xbytes >> 4, wstride = kUnitWBytes >> 4;
-      const uint32_t id_base = idesc_bf16(NP);
+      const uint32_t id_base = idesc_bf16_m256(NP);
+      const int NA = p.n_aslots;
       int sx = 0, sw = 0;
       uint32_t px = 0, pw = 0;
-      int ab = 0;                 // accumulator buffer of the current piece
-      int use0 = 0, use1 = 0;     // pieces already accumulated in buffers 0 / 1
-      int ks = (int)(u0 % p.n_ks);
-      for (long long u = u0; u < u1; ++u) {
-        const bool piece_first = (u == u0 || ks == 0);
-        const bool piece_last = (ks == p.n_ks - 1 || u == u1 - 1);
-        const int use = ab ? use1 : use0;
-        if (piece_first && use > 0) {
-          mbar_wait(&S.accempty[ab], (uint32_t)((use - 1) & 1));  // epilogue drained it
-          tc_fence_after();
-        }
-        const uint32_t d_base = tbase + (uint32_t)(ab * 2 * NP);
-        const uint32_t f0 = piece_first ? 0u : 1u;  // accumulate flag of the first k-block
-        mbar_wait(&S.xfull[sx], px);
-        const uint64_t xd = xdesc0 + (uint64_t)(sx * xstride);
-        if (has_w) {
-          mbar_wait(&S.wfull[sw], pw);
-          tc_fence_after();
-          const uint64_t wd = wdesc0 + (uint64_t)(sw * wstride);
-          mma_ss(d_base, wd, xd, id_base, f0);
+      int aslot = 0;
+      uint32_t aph = 0;
+      int ab = 0;
+      int use0 = 0, use1 = 0;
+      long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const long long tstart = clock64();
+      long long tq;
+      for (int pi = 0; pi < po.np; ++pi) {
+        long long pa, pb;
+        po.bounds(pi, pa, pb);
+        for (long long u = pa; u < pb; ++u) {
+          const bool piece_first = (u == pa);
+          const bool piece_last = (u == pb - 1);
+          const int use = ab ? use1 : use0;
+          if (piece_first && use > 0) {
+            mbar_wait_cluster(&S.accempty[ab], (uint32_t)((use - 1) & 1));  // both epilogues drained it
+            tc_fence_after();
+          }
+          const uint32_t d_base = tbase + (uint32_t)(ab * 2 * NP);
+          const uint32_t f0 = piece_first ? 0u : 1u;
+          tq = clock64();
+          mbar_wait_cluster(&S.xfull[sx], px);
+          prof[0] += clock64() - tq;
+          const uint64_t xd = xdesc0 + (uint64_t)(sx * xstride);
+          if (has_w) {
+            tq = clock64();
+            mbar_wait_cluster(&S.wfull[sw], pw);
+            prof[1] += clock64() - tq;
+            tq = clock64();
+            tc_fence_after();
+            const uint64_t wd = wdesc0 + (uint64_t)(sw * wstride);
+            mma2_ss(d_base, wd, xd, id_base, f0);
 #pragma unroll
-          for (int j = 1; j < 8; ++j) mma_ss(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
-          tc_commit(&S.wempty[sw]);  // weight tile free once these MMAs complete
-          if (++sw == p.nw) { sw = 0; pw ^= 1; }
+            for (int j = 1; j < 8; ++j) mma2_ss(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
+            tc2_commit(&S.wempty[sw]);
+            if (++sw == p.nw) { sw = 0; pw ^= 1; }
+            prof[2] += clock64() - tq;
+          }
+          for (int q = 0; q < p.n_seg; ++q) {
+            tq = clock64();
+            mbar_wait_cluster(&S.afull[aslot], aph);
+            prof[3] += clock64() - tq;
+            tq = clock64();
+            tc_fence_after();
+            const int win0 = S.segs[q].win0;
+            const uint32_t id = idesc_bf16_m256(S.segs[q].winN);
+            const uint32_t dd = d_base + (uint32_t)(NP + win0);
+            const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
+            // B rows of the expert's windows: window w's half lives at 1 KiB... (w * 2048 B) in each CTA
+            const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
+            mma2_ts(dd, a0, bd, id, f0);
+#pragma unroll
+            for (int j = 1; j < 8; ++j) mma2_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
+            tc2_commit(&S.aempty[aslot]);
+            if (++aslot == NA) { aslot = 0; aph ^= 1; }
+            prof[4] += clock64() - tq;
+            prof[7]++;
+          }
+          tc2_commit(&S.xempty[sx]);
+          if (++sx == p.nx) { sx = 0; px ^= 1; }
+          if (piece_last) {
+            tc2_commit(&S.accfull[ab]);
+            if (ab) ++use1; else ++use0;
+            if (p.n_acc == 2) ab ^= 1;
+          }
         }
-        tc_commit(&S.xempty[sx]);
-        if (++sx == p.nx) { sx = 0; px ^= 1; }
-        if (piece_last) {
-          tc_commit(&S.accfull[ab]);
-          if (ab) ++use1; else ++use0;
-          if (p.n_acc == 2) ab ^= 1;
-        }
-        if (++ks == p.n_ks) ks = 0;
-        if (u == u0) MESW_STAMP(2);
       }
       MESW_STAMP(3);
+      prof[6] = clock64() - tstart;
+      if (p.tbuf)
+        for (int i = 0; i < 8; ++i) p.tbuf[4096 * 8 + (size_t)blockIdx.x * 16 + i] = prof[i];
     }
   } else if (warp < kEpiWarp0) {
-    // ===================== dequant groups: codes -> TMEM A -> delta MMAs =====================
-    // Group g owns the jobs of experts q with q % 2 == g: its 128 threads (thread m =
-    // output channel m) expand the job's codes for all 128 k into bf16 A rows in TMEM,
-    // then one elected thread of the group issues the job's 8 tcgen05.mma (A from TMEM,
-    // B = the x rows of the expert's 16-token window) and commits them.  No handshake
-    // with the base-MMA warp: the groups and the MMA warp only meet at the x-tile release
-    // and at the per-piece accumulator barriers.
+    // ===================== dequant groups: own codes -> own TMEM A rows =====================
     const int grp = (warp - kDqWarp0) >> 2;
-    const int quarter = warp & 3;            // TMEM lanes [32*quarter, +32)
-    const int mrow = quarter * 32 + lane;    // output channel within the column group
-    const int gtid = ((warp - kDqWarp0) & 3) * 32 + lane;
+    const int quarter = warp & 3;
+    const int mrow = quarter * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-    const int NAW = p.n_aslots / kDqGroups;  // A slots per group
-    constexpr int WPJ = 2 * CHB / 4;         // code words per job per thread (both k-halves)
-    constexpr int MJ = 32 / WPJ;             // own jobs per chunk held in registers (host agrees)
-    const uint64_t xdesc0 = smem_desc(smem_u32(ring + p.xo));
-    const uint32_t xstride = (uint32_t)p.xbytes >> 4;
-    int sc = 0, sx = 0;
-    uint32_t pc = 0, px = 0;
-    long long job = 0;   // global job counter (jobs = (unit, segment) pairs)
-    long long mine = 0;  // jobs handled by this group so far
-    int ab = 0, use0 = 0, use1 = 0;
-    int ks = (int)(u0 % p.n_ks);
-    for (long long u = (p.n_seg > 0 ? u0 : u1); u < u1; ++u) {  // idle without experts
-      const bool piece_first = (u == u0 || ks == 0);
-      const bool piece_last = (ks == p.n_ks - 1 || u == u1 - 1);
-      const uint32_t d_delta = tbase + (uint32_t)(ab * 2 * NP + NP);
-      const uint32_t f0 = piece_first ? 0u : 1u;
-      bool waited_acc = !(piece_first && (ab ? use1 : use0) > 0);
-      bool waited_x = false;
-      const uint64_t xd = xdesc0 + (uint64_t)(sx * xstride);
-      for (int ch = 0; ch < p.n_chunks; ++ch) {
-        const int sg0 = ch * p.segs_per_chunk;
-        const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-        mbar_wait(&S.cfull[sc], pc);
-        const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
-        uint32_t cw[MJ][WPJ];
-        int own[MJ];
-        int nown = 0;
+    const int NA = p.n_aslots;
+    constexpr int WPJ = 2 * CHB / 4;
+    constexpr int MJ = 32 / WPJ;
+    int sc = 0;
+    uint32_t pc = 0;
+    int jpar = 0, jslot = 0, juse = 0;
+    for (int pi = 0; pi < (p.n_seg > 0 ? po.np : 0); ++pi) {
+      long long pa, pb;
+      po.bounds(pi, pa, pb);
+      for (long long u = pa; u < pb; ++u) {
+        for (int ch = 0; ch < p.n_chunks; ++ch) {
+          const int sg0 = ch * p.segs_per_chunk;
+          const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
+          const int off = (grp - jpar + kDqGroups) % kDqGroups;
+          mbar_wait(&S.cfull[sc], pc);
+          const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
+          uint32_t cw[MJ][WPJ];
 #pragma unroll
-        for (int jq = 0; jq < MJ; ++jq) own[jq] = -1;
-        for (int q = sg0; q < sg1; ++q) {
-          if (q % kDqGroups != grp) continue;  // expert q always handled by group q % 2:
-                                               // one issuing thread per accumulator window
-                                               // keeps the k-order of its MMAs fixed
+          for (int jq = 0; jq < MJ; ++jq) {
+            const int q = sg0 + jq * kDqGroups + off;
+            if (q < sg1) {
+              const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
 #pragma unroll
-          for (int jq = 0; jq < MJ; ++jq)
-            if (jq == nown) own[jq] = q;
-          ++nown;
-        }
+              for (int kh = 0; kh < 2; ++kh)
 #pragma unroll
-        for (int jq = 0; jq < MJ; ++jq) {
-          if (own[jq] >= 0) {
-            const uint8_t* cb = cst + (size_t)(own[jq] - sg0) * CB;
-#pragma unroll
-            for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-              for (int v = 0; v < CHB / 16; ++v) {
-                const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
-                const int w0 = kh * (CHB / 4) + 4 * v;
-                cw[jq][w0] = t4.x; cw[jq][w0 + 1] = t4.y; cw[jq][w0 + 2] = t4.z; cw[jq][w0 + 3] = t4.w;
-              }
+                for (int v = 0; v < CHB / 16; ++v) {
+                  const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
+                  const int w0 = kh * (CHB / 4) + 4 * v;
+                  cw[jq][w0] = t4.x; cw[jq][w0 + 1] = t4.y; cw[jq][w0 + 2] = t4.z; cw[jq][w0 + 3] = t4.w;
+                }
+            }
           }
-        }
-        mbar_arrive(&S.cempty[sc]);  // every thread: release orders its own smem reads
-        if (++sc == p.nc) { sc = 0; pc ^= 1; }
+          mbar_arrive(&S.cempty[sc]);  // every thread: release orders its own smem reads
+          if (++sc == p.nc) { sc = 0; pc ^= 1; }
 #pragma unroll
-        for (int jq = 0; jq < MJ; ++jq) {
-          if (own[jq] >= 0) {
-            const int q = own[jq];
-            const int aslot = grp * NAW + (int)(mine % NAW);
-            const long long use = mine / NAW;
-            if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
-            const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
+          for (int jq = 0; jq < MJ; ++jq) {
+            const int q = sg0 + jq * kDqGroups + off;
+            if (q < sg1) {
+              const int sj = jslot + (q - sg0);
+              const int aslot = sj % NA;
+              const int use = juse + sj / NA;
+              if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
+              const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {  // one k-half (32 columns) at a time
-              uint32_t r[32];
-              if (p.dbg & 1) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) r[i] = cw[jq][i % WPJ];
-              } else {
+              for (int kh = 0; kh < 2; ++kh) {
+                uint32_t r[32];
                 dequant_chunk<DB>(&cw[jq][kh * (CHB / 4)], r);
+                tmem_st32(a0 + lane_addr + 32 * kh, r);
               }
-              if (!(p.dbg & 4)) tmem_st32(a0 + lane_addr + 32 * kh, r);
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {  // 4 warps of each CTA -> leader's afull (8 arrivals)
+                if (rank == 0) mbar_arrive(&S.afull[aslot]);
+                else mbar_arrive_cta(&S.afull[aslot], 0);
+              }
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            named_bar_sync(2 + grp, 128);  // the job's A rows are all in TMEM
-            if (gtid == 0) {
-              if (!waited_acc) {  // previous piece in this buffer drained by the epilogue
-                const int uacc = ab ? use1 : use0;
-                mbar_wait(&S.accempty[ab], (uint32_t)((uacc - 1) & 1));
-                waited_acc = true;
-              }
-              if (!waited_x) {
-                mbar_wait(&S.xfull[sx], px);
-                waited_x = true;
-              }
-              tc_fence_after();
-              const SegDesc& sd = S.segs[q];
-              const uint32_t id = idesc_bf16(sd.winN);
-              const uint32_t dd = d_delta + (uint32_t)sd.win0;
-              const uint64_t bd = xd + (uint64_t)((sd.win0 >> 3) * (kXRowGroupBytes >> 4));
-              if (!(p.dbg & 2)) {
-                mma_ts(dd, a0, bd, id, f0);
-#pragma unroll
-                for (int j = 1; j < 8; ++j) mma_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
-              }
-              tc_commit(&S.aempty[aslot]);
-            }
-            ++mine;
           }
+          jpar = (jpar + (sg1 - sg0)) % kDqGroups;
+          jslot += sg1 - sg0;
+          while (jslot >= NA) { jslot -= NA; ++juse; }
         }
-        job += sg1 - sg0;
       }
-      if (gtid == 0) {
-        if (!waited_acc) {
-          const int uacc = ab ? use1 : use0;
-          mbar_wait(&S.accempty[ab], (uint32_t)((uacc - 1) & 1));
-        }
-        if (!waited_x) mbar_wait(&S.xfull[sx], px);
-        tc_commit(&S.xempty[sx]);  // this group's MMAs on the x tile are done
-        if (piece_last) tc_commit(&S.accfull[ab]);
-      }
-      if (++sx == p.nx) { sx = 0; px ^= 1; }
-      if (piece_last) {
-        if (ab) ++use1; else ++use0;
-        if (p.n_acc == 2) ab ^= 1;
-      }
-      if (++ks == p.n_ks) ks = 0;
     }
   } else {
-    // ===================== epilogue warpgroup =====================
+    // ===================== epilogue warpgroup (own column group) =====================
     const int quarter = warp & 3;
     const int mrow = quarter * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     const int gtid = (warp - kEpiWarp0) * 32 + lane;  // 0..127
-    const int cg_first = (int)(u0 / p.n_ks);
+    const int cgp_first = (int)(u0 / p.n_ks);
     int ab = 0;
     int acc_use[2] = {0, 0};
-    long long u = u0;
-    while (u < u1) {
-      // the piece is the run of this CTA's units inside one column group
-      const int cg = (int)(u / p.n_ks);
-      const long long cg_end = (long long)(cg + 1) * p.n_ks;
-      const long long piece_end = cg_end < u1 ? cg_end : u1;
-      const bool whole = (u == (long long)cg * p.n_ks) && (piece_end == cg_end);
-      // accumulator-independent operands first (overlaps the main loop)
+    for (int pi = 0; pi < po.np; ++pi) {
+      long long u, piece_end;
+      po.bounds(pi, u, piece_end);
+      const int cgp = po.cg_of(pi);
+      const int cg = 2 * cgp + (int)rank;
+      const long long cg_end = (long long)(cgp + 1) * p.n_ks;
+      const bool whole = (u == (long long)cgp * p.n_ks) && (piece_end == cg_end);
       const bool fast = gather_salient_x(p, S, cg, gtid);
       EpiPre pre;
       epi_prefetch(p, S, cg, mrow, 0, fast, pre);
       mbar_wait(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
       tc_fence_after();
+      if (gtid == 0 && pi == po.np - 1) MESW_STAMP(5);
       const uint32_t acc = tbase + lane_addr + (uint32_t)(ab * 2 * NP);
-      if (p.dbg & 8) {
-        // timing experiment: skip the epilogue
-      } else if (whole) {
+      if (whole) {
         for (int t0 = 0; t0 < NP; t0 += 16) {
           float vb[16], vd[16];
           if (has_w) {
-            tmem_ld16(acc + (uint32_t)t0, vb);
+            tmem_ld8(acc + (uint32_t)(t0 / 2), vb);           // rows t0..t0+7 (first half)
+            tmem_ld8(acc + (uint32_t)(HP + t0 / 2), vb + 8);  // rows t0+8..t0+15 (second half)
           } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) vb[i] = 0.f;  // delta-only: D_base never written
           }
-          tmem_ld16(acc + (uint32_t)(NP + t0), vd);
-          const EpiPre cur = pre;
+          const int sg = S.tok2seg[t0];
+          if (sg >= 0) {
+            const SegDesc& sd = S.segs[sg];
+            const int dw = (t0 - sd.win0) / 2;  // window's column inside the expert's D range
+            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + dw), vd);
+            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + sd.winN / 2 + dw), vd + 8);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vd[i] = 0.f;
+          }
+          epi_store16(p, S, cg, mrow, t0, vb, vd, fast, pre);
           if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
-          epi_store16(p, S, cg, mrow, t0, vb, vd, fast, cur);
         }
       } else {
-        const int slot = 2 * c + (cg == cg_first ? 0 : 1);
+        const int slot = 2 * c + (cgp == cgp_first ? 0 : 1);
         const size_t slot_floats = (size_t)2 * NP * kUnitN;
         float* mine = p.ws + (size_t)slot * slot_floats;
         for (int t0 = 0; t0 < 2 * NP; t0 += 16) {
@@ -673,61 +794,80 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           for (int i = 0; i < 16; ++i) __stcg(mine + (size_t)(t0 + i) * kUnitN + mrow, v[i]);
         }
       }
-      // accumulators consumed -> the MMA warp may reuse this buffer
+      // accumulators consumed -> the leader may reuse this buffer
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.accempty[ab]);
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(&S.accempty[ab]);
+        else mbar_arrive_cta(&S.accempty[ab], 0);
+      }
+      if (gtid == 0 && pi == po.np - 1) MESW_STAMP(6);
       acc_use[ab]++;
       if (p.n_acc == 2) ab ^= 1;
-      if (!whole && !(p.dbg & 8)) {
+      if (!whole) {
         __threadfence();
         named_bar_sync(1, 128);
-        const long long first_u = (long long)cg * p.n_ks, last_u = first_u + p.n_ks - 1;
-        const int c_first = unit_owner(first_u, p.T, p.G), c_last = unit_owner(last_u, p.T, p.G);
+        // contributors to this column group: the pairs owning its first/last unit
+        const long long first_u = (long long)cgp * p.n_ks, last_u = first_u + p.n_ks - 1;
+        const int p_first = unit_owner(first_u, T2, (int)G2), p_last = unit_owner(last_u, T2, (int)G2);
         if (gtid == 0) {
           const int prev = atomicAdd(&p.counters[cg], 1);
-          S.flag = (prev == c_last - c_first) ? 1 : 0;
+          S.flag = (prev == p_last - p_first) ? 1 : 0;
         }
         named_bar_sync(1, 128);
         if (S.flag) {
           __threadfence();
           const size_t slot_floats = (size_t)2 * NP * kUnitN;
           for (int t0 = 0; t0 < NP; t0 += 16) {
+            const int sg = S.tok2seg[t0];
+            int cb0 = t0 / 2, cb1 = HP + t0 / 2, cd0 = -1, cd1 = -1;
+            if (sg >= 0) {
+              const SegDesc& sd = S.segs[sg];
+              const int dw = (t0 - sd.win0) / 2;
+              cd0 = NP + sd.win0 + dw;
+              cd1 = NP + sd.win0 + sd.winN / 2 + dw;
+            }
             float vb[16], vd[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) vb[i] = vd[i] = 0.f;
-            for (int cc = c_first; cc <= c_last; ++cc) {
-              const long long cu0 = (long long)cc * p.T / p.G;
-              const int s2 = 2 * cc + ((int)(cu0 / p.n_ks) == cg ? 0 : 1);
-              const float* src = p.ws + (size_t)s2 * slot_floats;
-              float lb[16], ld[16];
+            for (int pp = p_first; pp <= p_last; ++pp) {
+              const long long pu0 = (long long)pp * T2 / G2;
+              const int s2 = 2 * (2 * pp + (int)rank) + ((int)(pu0 / p.n_ks) == cgp ? 0 : 1);
+              const float* src = p.ws + (size_t)s2 * slot_floats + mrow;
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {  // all loads of the slot in flight together
-                lb[i] = __ldcg(src + (size_t)(t0 + i) * kUnitN + mrow);
-                ld[i] = __ldcg(src + (size_t)(NP + t0 + i) * kUnitN + mrow);
+              for (int i = 0; i < 8; ++i) {
+                vb[i] += __ldcg(src + (size_t)(cb0 + i) * kUnitN);
+                vb[8 + i] += __ldcg(src + (size_t)(cb1 + i) * kUnitN);
               }
+              if (cd0 >= 0) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) { vb[i] += lb[i]; vd[i] += ld[i]; }
+                for (int i = 0; i < 8; ++i) {
+                  vd[i] += __ldcg(src + (size_t)(cd0 + i) * kUnitN);
+                  vd[8 + i] += __ldcg(src + (size_t)(cd1 + i) * kUnitN);
+                }
+              }
             }
-            const EpiPre cur = pre;
+            if (!has_w) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) vb[i] = 0.f;
+            }
+            epi_store16(p, S, cg, mrow, t0, vb, vd, fast, pre);
             if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
-            epi_store16(p, S, cg, mrow, t0, vb, vd, fast, cur);
           }
           if (gtid == 0) p.counters[cg] = 0;  // self-reset for the next launch
         }
       }
       named_bar_sync(1, 128);  // xsal / flag reuse by the next piece
-      if (gtid == 0) MESW_STAMP(u == u0 ? 4 : 5);
-      u = piece_end;
+      if (gtid == 0) MESW_STAMP(pi == po.np - 1 ? 7 : 4);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) MESW_STAMP(6);
+  cluster_sync_all();  // the peer's MMAs / TMEM reads are complete before deallocation
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
   }
 }
 
@@ -740,7 +880,20 @@ int launch(const LinearParams& p, size_t smem, cudaStream_t stream) {
     if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
     configured = true;
   }
-  me_linear_tc_kernel<DB><<<p.G, kThreads, smem, stream>>>(p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // CTA pairs for cta_group::2
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, me_linear_tc_kernel<DB>, p);
+  if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("me_linear");
 }
 
@@ -755,7 +908,7 @@ static unsigned long long* g_tbuf = nullptr;
 // Debug: copy the last MESW_TIMING launch's per-CTA globaltimer stamps (8 per CTA).
 extern "C" int mesw_debug_timing_copy(unsigned long long* h_out, int n_ctas) {
   if (!g_tbuf) return mesw_fail(MESW_ERR_VALUE, "no timing buffer (set MESW_TIMING)");
-  cudaError_t e = cudaMemcpy(h_out, g_tbuf, (size_t)n_ctas * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpy(h_out, g_tbuf, (size_t)16 * 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? MESW_OK : mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
 }
 
@@ -793,7 +946,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
 
   LinearParams p{};
   p.x = a->x; p.B = a->B; p.NP = pad16(a->B); p.m = a->m; p.n = a->n;
-  p.n_cg = n_pad / kUnitN; p.n_ks = m_pad / kUnitK;
+  p.n_cg = ((n_pad + 2 * kUnitN - 1) / (2 * kUnitN)) * 2; p.n_ks = m_pad / kUnitK;
   p.w = reinterpret_cast<const uint8_t*>(a->w);
   p.table = a->expert_table;
   p.n_seg = a->n_segments;
@@ -804,18 +957,20 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   p.residual = a->residual; p.ld_res = a->ld_res;
   p.ws = reinterpret_cast<float*>(a->workspace);
   p.counters = a->counters;
-  p.T = (long long)p.n_cg * p.n_ks;
+  if (p.n_cg % 2) return mesw_fail(MESW_ERR_VALUE, "device buffers must cover an even number of 128-column groups");
+  p.T = (long long)(p.n_cg / 2) * p.n_ks;  // pair units (2 column groups x 1 k-step)
   p.activation = a->activation;
   {
     const char* e = getenv("MESW_DBG");
     p.dbg = e ? atoi(e) : 0;
     if (getenv("MESW_TIMING")) {
-      if (!g_tbuf) cudaMalloc(&g_tbuf, 8 * 4096 * sizeof(unsigned long long));
+      if (!g_tbuf) cudaMalloc(&g_tbuf, 16 * 4096 * sizeof(unsigned long long));
       p.tbuf = g_tbuf;
     }
   }
-  const int want = a->num_ctas > 0 ? a->num_ctas : sms;
-  p.G = (int)((long long)want < p.T ? want : p.T);
+  // n_cg here = column groups of the device buffers (a->n_alloc); pairs of CTAs (clusters of 2)
+  const int want = (a->num_ctas > 0 ? a->num_ctas : sms) / 2;
+  p.G = 2 * (int)((long long)(want > 0 ? want : 1) < p.T ? (want > 0 ? want : 1) : p.T);
   if (a->workspace_bytes < mesw_linear_workspace_bytes(a->B, p.G) || !a->workspace || !a->counters)
     return mesw_fail(MESW_ERR_VALUE, "workspace too small");
 
@@ -825,7 +980,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   const int max_chunk = (db == 2 ? 4 : (db == 4 ? 2 : 1)) * kDqGroups;  // jobs per code chunk
   p.segs_per_chunk = p.n_seg == 0 ? 1 : (p.n_seg < max_chunk ? p.n_seg : max_chunk);
   p.n_chunks = p.n_seg == 0 ? 0 : (p.n_seg + p.segs_per_chunk - 1) / p.segs_per_chunk;
-  p.xbytes = p.NP * kUnitK * 2;
+  p.xbytes = (p.NP / 2) * kUnitK * 2;  // this CTA's half of the activation tile
   p.cbytes = p.segs_per_chunk * CB;
   const size_t budget = 232448 - ring_offset();
   // ring depths: prefer (x 3, codes 3, weights >= 3); shrink x/codes first when rows are many

@@ -62,7 +62,9 @@ class LinearGeometry:
 
     @property
     def n_pad(self) -> int:
-        return sum(_ceil(nb) for nb in self.block_n)
+        """Device columns: blocks padded to 128, total padded to 256 (the fused kernel's
+        CTA pairs own two 128-column groups each)."""
+        return _ceil(sum(_ceil(nb) for nb in self.block_n), 2 * TILE)
 
     @property
     def n(self) -> int:

@@ -83,10 +83,10 @@ def test_salient_tables_layout():
     art_blocks = [compress.deserialize_artifact(om.serialize_artifact(
         {"model_id": "x", "domain": "d", "base_digest": "0", "layer_count": 1}, [b])).layers[0] for b in blocks]
     geom = LinearGeometry(200, (300, 128, 70))
-    assert geom.col_base == (0, 384, 512) and geom.n_pad == 640 and geom.n == 582
+    assert geom.col_base == (0, 384, 512) and geom.n_pad == 768 and geom.n == 582
     off, idx, rows = build_salient_tables(art_blocks, geom)
     off, idx, rows = off.numpy(), idx.numpy(), rows.numpy().view(np.uint16)
-    assert off.tolist() == [0, 5, 10, 15, 15, 18]
+    assert off.tolist() == [0, 5, 10, 15, 15, 18, 18]
     for cg in range(5):
         for r in range(off[cg], off[cg + 1]):
             b = 0 if cg < 3 else 2

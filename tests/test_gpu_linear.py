@@ -247,5 +247,6 @@ def test_pack_x_roundtrip_and_layout():
         NP = canonical_rows(B)
         flat = xc.cpu()
         t, k = B - 1, m - 1
-        idx = (k // 128) * NP * 128 + (t // 8) * 1024 + ((k % 128) // 8) * 64 + (t % 8) * 8 + k % 8
+        idx = ((k // 128) * NP * 128 + ((t // 8) % 2) * (NP // 2) * 128 + (t // 16) * 1024
+               + ((k % 128) // 8) * 64 + (t % 8) * 8 + k % 8)
         assert flat[idx] == x[t, k].cpu()

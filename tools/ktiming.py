@@ -20,14 +20,22 @@ for _ in range(3): plan()
 torch.cuda.synchronize()
 plan(); torch.cuda.synchronize()
 G = min(148, (n // 128) * (m // 128))
-buf = np.zeros(G * 8, np.uint64)
+G -= G % 2
+buf = np.zeros(16 * 4096, np.uint64)
 _lib.check(L.mesw_debug_timing_copy(buf.ctypes.data, G))
-t = buf.reshape(G, 8).astype(np.int64)
+t = buf[:G * 8].reshape(G, 8).astype(np.int64)
+prof = buf[4096 * 8:4096 * 8 + G * 16].reshape(G, 2, 8).astype(np.int64)
 t0 = t[:, 0].min()
-names = ["start", "prod_done", "mma_unit0", "mma_done", "epi_piece0", "epi_last", "cta_end"]
+names = ["start", "prod_done", "mma_unit0", "mma_done", "epi_first", "last_accfull", "last_tmem", "last_end"]
 print(f"m={m} n={n} E={E} rows={rows}  (us from first CTA start)")
 for i, nm in enumerate(names):
     v = (t[:, i] - t0) / 1e3
     v = v[t[:, i] > 0]
     if v.size:
         print(f"  {nm:12s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f}")
+
+pm = ["wait_x", "wait_w", "base_issue", "wait_afull", "delta_issue", "wait_accempty", "total", "jobs"]
+pd = ["wait_cfull", "wait_aempty", "dequant+st", "-", "-", "-", "total", "jobs"]
+lead = prof[0::2, 0, :]
+print("  mma   ", " ".join(f"{pm[i]}={np.median(lead[:, i]):.0f}" for i in range(8)))
+print("  deq0  ", " ".join(f"{pd[i]}={np.median(prof[:, 1, i]):.0f}" for i in range(8) if pd[i] != "-"))

@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ int g_swz;
 __device__ __forceinline__ uint64_t sdesc(uint32_t a) {
+  if (g_swz)  // SWIZZLE_128B K-major: SBO = 1024 B (8 rows x 128 B), LBO ignored
+    return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | (1ull << 46) | (2ull << 61);
   return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)8 << 16) | ((uint64_t)128 << 32) | (1ull << 46);
 }
 __device__ __forceinline__ uint32_t idesc(int M, int N) {
@@ -14,7 +17,11 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
   asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
-__global__ void bench(int M, int N, int R, unsigned long long* out) {
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__global__ void bench(int M, int N, int R, unsigned long long* out, int ts) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t tb;
   __shared__ __align__(8) uint64_t bar;
@@ -41,8 +48,28 @@ __global__ void bench(int M, int N, int R, unsigned long long* out) {
     long long c0 = clock64();
     if (threadIdx.x == 32) {
       for (int i = 0; i < R; i += 8) {
+        if (ts == 1) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) mma_ss(t, da + 16 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+          for (int j = 0; j < 8; ++j) mma_ts(t, t + 256 + 8 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+        } else if (ts == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mma_ss(t, da + (g_swz ? 2 * (j & 3) + 64 * (j >> 2) : 16 * j), db + (g_swz ? 2 * (j & 3) + 64 * (j >> 2) : 16 * j), id, (i | j) ? 1u : 0u);
+        } else if (ts == 2) {  // alternate accumulators every 8 (SS)
+          const uint32_t dd = t + ((i >> 3) & 1) * 64;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mma_ss(dd, da + 16 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+        } else if (ts == 3) {  // alternate SS / TS every 8, separate accumulators
+          if ((i >> 3) & 1) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mma_ts(t + 64, t + 256 + 8 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mma_ss(t, da + 16 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+          }
+        } else {  // ts == 4: alternate accumulators every MMA (SS)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mma_ss(t + (j & 1) * 64, da + 16 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     }
@@ -62,11 +89,16 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 32);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
-  const int R = 4096;
-  for (int rep = 0; rep < 2; ++rep)
-    for (int M : {64, 128})
-      for (int N : {16, 64, 128, 256}) {
-        bench<<<1, 128, 131072>>>(M, N, R, d);
+  const int R = 4096;  // multiple of 16
+  const char* nm[] = {"SS", "TS", "SS-alt8", "SS/TS-alt8", "SS-alt1"};
+  for (int swz = 0; swz < 2; ++swz) {
+  cudaMemcpyToSymbol(g_swz, &swz, sizeof(int));
+  printf("swizzle %d\n", swz);
+  for (int ts = 0; ts < 2; ++ts)
+    for (int M : {128})
+      for (int N : {16, 48}) {
+        bench<<<1, 128, 131072>>>(M, N, R, d, ts);
+        printf("%-11s ", nm[ts]);
         unsigned long long h[3];
         cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
         double macs = (double)M * N * 16;
@@ -74,6 +106,7 @@ int main() {
                M, N, (double)h[0] / R, (double)h[1] / R, (double)h[2] / R, macs / ((double)h[1] / R),
                (double)h[1] / h[2]);
       }
+  }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
