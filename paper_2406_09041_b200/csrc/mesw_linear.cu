@@ -24,6 +24,8 @@
 
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "mesw_common.cuh"
 #include "mesw_host.h"
 #include "mesw_layout.cuh"
@@ -31,9 +33,9 @@
 namespace mesw {
 
 constexpr int kDqGroups = 2;  // dequant warpgroups: group g expands k-half g of every job
-// warp roles: 0 weight-tile producer, 1 base-MMA issuer, 2 x-tile producer, 3 code producer,
-// 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
-constexpr int kWProdWarp = 0, kMmaWarp = 1, kXProdWarp = 2, kCProdWarp = 3;
+// warp roles: 0 weight-tile producer, 1-2 MMA issuers, 3 activation + code producer, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
+constexpr int kWProdWarp = 0, kMmaWarp = 1, kMma2Warp = 2, kCProdWarp = 3;
+constexpr int kMaxIssuers = 2;
 constexpr int kDqWarp0 = 4, kEpiWarp0 = kDqWarp0 + 4 * kDqGroups;
 constexpr int kThreads = (kEpiWarp0 + 4) * 32;  // 16 warps
 constexpr int kTmemCols = 512;
@@ -43,6 +45,7 @@ constexpr int kMaxRows = 192;  // padded token rows per launch (TMEM: 2 * rows <
 constexpr int kMaxStages = 8;
 constexpr int kXRowGroupBytes = 2048;  // 8 token rows x 16 k-chunks x 16 B
 constexpr int kSalFast = 16;           // salient rows per column group handled from smem
+constexpr int kRedBatch = 1;           // stream-K partials loaded per L2 round trip
 
 // Element index of x[t][k] in the canonical activation layout (see mesw.h): per 128-wide
 // k-step, two halves h = (t/8)%2 (rows 0-7 / 8-15 of every 16-row window), each a
@@ -87,6 +90,7 @@ struct LinearParams {
   int nc, co, cbytes, segs_per_chunk, n_chunks;
   // tensor memory: n_acc accumulator buffers of 2*NP columns, A ring from a_col0
   int n_acc, n_aslots, a_col0;
+  int n_iss;  // MMA issuer threads (a tcgen05.mma stream runs ~60-85 cycles/instr per issuer)
   unsigned long long* tbuf;  // MESW_TIMING: per-CTA globaltimer stamps
   int dbg;  // perf experiments: bit0 skip dequant math, bit1 skip delta MMAs, bit2 skip tcgen05.st
 };
@@ -101,6 +105,7 @@ struct Smem {
   int flag;
   int tok2seg[kMaxRows];
   SegDesc segs[MESW_MAX_SEGMENTS];
+  int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
   float xsal[kMaxRows][16];  // x[t][salient idx r] of the current column group (k <= 16 fast path)
 };
 
@@ -175,6 +180,14 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+// Relaxed variant for "data already complete" signals (TMA complete_tx observed, or
+// tcgen05.wait::st retired): orders nothing itself, avoids the cluster-scope release fence.
+__device__ __forceinline__ void mbar_arrive_cta_relaxed(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
 // Wait with cluster-scope acquire (barriers that receive arrivals from the peer CTA).
@@ -335,11 +348,16 @@ __device__ __forceinline__ int unit_owner(long long u, long long T, int G) {
 // overlap the main loop.  Returns false if some segment has > kSalFast salient rows in
 // cg (then the epilogue reads them from global memory).
 __device__ __forceinline__ bool gather_salient_x(const LinearParams& p, Smem& S, int cg, int gtid) {
-  bool fast = true;
-  for (int q = 0; q < p.n_seg; ++q) {
+  for (int q = gtid; q < p.n_seg; q += 128) {
     const SegDesc& sd = S.segs[q];
-    if (sd.sal_off[cg + 1] - sd.sal_off[cg] > kSalFast) fast = false;
+    const int r0 = sd.sal_off[cg];
+    S.sal_r0[q] = r0;
+    S.sal_k[q] = sd.sal_off[cg + 1] - r0;
   }
+  named_bar_sync(1, 128);
+  bool fast = true;
+  for (int q = 0; q < p.n_seg; ++q)
+    if (S.sal_k[q] > kSalFast) fast = false;
   if (fast && p.n_seg > 0) {
     const int total = p.B * kSalFast;
     for (int i0 = gtid; i0 < total; i0 += 128 * 4) {
@@ -351,11 +369,8 @@ __device__ __forceinline__ bool gather_salient_x(const LinearParams& p, Smem& S,
         if (i < total) {
           const int t = i / kSalFast, r = i % kSalFast;
           const int sg = S.tok2seg[t];
-          if (sg >= 0) {
-            const SegDesc& sd = S.segs[sg];
-            const int r0 = sd.sal_off[cg];
-            if (r < sd.sal_off[cg + 1] - r0) v[k] = bf16_to_f32(p.x[xc_index(t, sd.sal_idx[r0 + r], p.NP)]);
-          }
+          if (sg >= 0 && r < S.sal_k[sg])
+            v[k] = bf16_to_f32(p.x[xc_index(t, S.segs[sg].sal_idx[S.sal_r0[sg] + r], p.NP)]);
         }
       }
 #pragma unroll
@@ -393,7 +408,7 @@ __device__ __forceinline__ void epi_prefetch(const LinearParams& p, const Smem& 
     const SegDesc& sd = S.segs[e.sg];
     e.sj = sd.steps[j];
     if (fast) {
-      const int r0 = sd.sal_off[cg], k = sd.sal_off[cg + 1] - r0;
+      const int r0 = S.sal_r0[e.sg], k = S.sal_k[e.sg];  // smem: no dependent global round trip
 #pragma unroll
       for (int r = 0; r < kSalFast; ++r)
         if (r < k) e.R[r] = __half2float(__ushort_as_half(sd.sal_rows[(size_t)(r0 + r) * kUnitN + m]));
@@ -474,11 +489,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
 
   if (threadIdx.x == 0) {
     const uint32_t peer_relay = rank == 0 ? 2 : 1;  // leader: own tile + peer relay
-    for (int i = 0; i < p.nx; ++i) { mbar_init(&S.xfull[i], peer_relay); mbar_init(&S.xempty[i], 1); }
+    for (int i = 0; i < p.nx; ++i) { mbar_init(&S.xfull[i], peer_relay); mbar_init(&S.xempty[i], p.n_iss); }
     for (int i = 0; i < p.nw; ++i) { mbar_init(&S.wfull[i], peer_relay); mbar_init(&S.wempty[i], 1); }
     for (int i = 0; i < p.nc; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 128 * kDqGroups); }
     for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 8); mbar_init(&S.aempty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], 1); mbar_init(&S.accempty[i], 8); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], p.n_iss); mbar_init(&S.accempty[i], 8); }
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -511,13 +526,13 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   const bool has_w = p.w != nullptr;
   if (threadIdx.x == 0) MESW_STAMP(0);
 
-  if (warp == kWProdWarp || warp == kXProdWarp || warp == kCProdWarp) {
+  if (warp == kWProdWarp || warp == kCProdWarp) {
     // ===================== producers (own column group / own x half) =====================
     uint64_t evict_first;  // weights / codes are streamed once: do not let them evict partials
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
-    int st = 0;
-    uint32_t ph = 0;
-    bool first = true;
+    int st = 0, sx = 0;
+    uint32_t ph = 0, px = 0;
+    bool first = true, xfirst = true;
     for (int pi = 0; pi < po.np; ++pi) {
       long long pa, pb;
       po.bounds(pi, pa, pb);
@@ -526,15 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       for (long long u = pa; u < pb; ++u) {
         const int ks = (int)(u - (long long)cgp * p.n_ks);
         const long long unit = (long long)cg * p.n_ks + ks;  // this CTA's unit
-        if (warp == kXProdWarp) {
-          if (lane == 0) {
-            if (!first) mbar_wait(&S.xempty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&S.xfull[st], (uint32_t)p.xbytes);
-            bulk_g2s(ring + p.xo + (size_t)st * p.xbytes, p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK,
-                     p.xbytes, &S.xfull[st]);
-            if (++st == p.nx) { st = 0; ph ^= 1; first = false; }
-          }
-        } else if (warp == kWProdWarp) {
+        if (warp == kWProdWarp) {
           if (lane == 0 && has_w) {
             if (!first) mbar_wait(&S.wempty[st], ph ^ 1);
             mbar_arrive_expect_tx(&S.wfull[st], kUnitWBytes);
@@ -542,28 +549,31 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
                           &S.wfull[st], evict_first);
             if (++st == p.nw) { st = 0; ph ^= 1; first = false; }
           }
-        } else {
+        } else if (lane == 0) {
+          // activation half-tile, then this unit's code chunks (one thread: no divergent spinning)
+          if (!xfirst) mbar_wait(&S.xempty[sx], px ^ 1);
+          mbar_arrive_expect_tx(&S.xfull[sx], (uint32_t)p.xbytes);
+          bulk_g2s(ring + p.xo + (size_t)sx * p.xbytes, p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK,
+                   p.xbytes, &S.xfull[sx]);
+          if (++sx == p.nx) { sx = 0; px ^= 1; xfirst = false; }
           for (int ch = 0; ch < p.n_chunks; ++ch) {
             const int sg0 = ch * p.segs_per_chunk;
             const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-            if (lane == 0) {
-              if (!first) mbar_wait(&S.cempty[st], ph ^ 1);
-              mbar_arrive_expect_tx(&S.cfull[st], (uint32_t)(sg1 - sg0) * CB);
-            }
-            __syncwarp();
-            for (int q = sg0 + lane; q < sg1; q += 32)
+            if (!first) mbar_wait(&S.cempty[st], ph ^ 1);
+            mbar_arrive_expect_tx(&S.cfull[st], (uint32_t)(sg1 - sg0) * CB);
+            for (int q = sg0; q < sg1; ++q)
               bulk_g2s_hint(ring + p.co + (size_t)st * p.cbytes + (size_t)(q - sg0) * CB,
                             S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[st], evict_first);
-            __syncwarp();
             if (++st == p.nc) { st = 0; ph ^= 1; first = false; }
           }
         }
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaWarp || warp == kMma2Warp) {
+    const int role = warp - kMmaWarp;
     if (rank != 0) {
       // ===================== peer: relay "x / weight tile landed" to the leader =====================
-      if (lane == 0) {
+      if (role == 0 && lane == 0) {
         int sx = 0, sw = 0;
         uint32_t px = 0, pw = 0;
         for (int pi = 0; pi < po.np; ++pi) {
@@ -571,18 +581,23 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           po.bounds(pi, pa, pb);
           for (long long u = pa; u < pb; ++u) {
             mbar_wait(&S.xfull[sx], px);
-            mbar_arrive_cta(&S.xfull[sx], 0);
+            mbar_arrive_cta_relaxed(&S.xfull[sx], 0);
             if (++sx == p.nx) { sx = 0; px ^= 1; }
             if (has_w) {
               mbar_wait(&S.wfull[sw], pw);
-              mbar_arrive_cta(&S.wfull[sw], 0);
+              mbar_arrive_cta_relaxed(&S.wfull[sw], 0);
               if (++sw == p.nw) { sw = 0; pw ^= 1; }
             }
           }
         }
       }
-    } else if (lane == 0) {
-      // ===================== leader: issue every MMA of the pair =====================
+    } else if (lane == 0 && role < p.n_iss) {
+      // ===================== leader: issue the pair's MMAs =====================
+      // Issuer 0: base tile + odd segments; issuer 1: even segments (one issuer: everything).
+      // Each segment's delta accumulator is owned by exactly one issuer, so the k-ordered
+      // accumulate chain of every TMEM column range stays in one thread's issue order.
+      const bool do_base = has_w && role == 0;
+      const int seg_par = p.n_iss == 1 ? -1 : (role ^ 1);
       const uint64_t xdesc0 = smem_desc(smem_u32(ring + p.xo));
       const uint64_t wdesc0 = smem_desc(smem_u32(ring + p.wo));
       const uint32_t xstride = (uint32_t)p.xbytes >> 4, wstride = kUnitWBytes >> 4;
@@ -605,8 +620,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           const bool piece_last = (u == pb - 1);
           const int use = ab ? use1 : use0;
           if (piece_first && use > 0) {
+            tq = clock64();
             mbar_wait_cluster(&S.accempty[ab], (uint32_t)((use - 1) & 1));  // both epilogues drained it
             tc_fence_after();
+            prof[5] += clock64() - tq;
           }
           const uint32_t d_base = tbase + (uint32_t)(ab * 2 * NP);
           const uint32_t f0 = piece_first ? 0u : 1u;
@@ -614,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           mbar_wait_cluster(&S.xfull[sx], px);
           prof[0] += clock64() - tq;
           const uint64_t xd = xdesc0 + (uint64_t)(sx * xstride);
-          if (has_w) {
+          if (do_base) {
             tq = clock64();
             mbar_wait_cluster(&S.wfull[sw], pw);
             prof[1] += clock64() - tq;
@@ -629,24 +646,26 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             prof[2] += clock64() - tq;
           }
           for (int q = 0; q < p.n_seg; ++q) {
-            tq = clock64();
-            mbar_wait_cluster(&S.afull[aslot], aph);
-            prof[3] += clock64() - tq;
-            tq = clock64();
-            tc_fence_after();
-            const int win0 = S.segs[q].win0;
-            const uint32_t id = idesc_bf16_m256(S.segs[q].winN);
-            const uint32_t dd = d_base + (uint32_t)(NP + win0);
-            const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
-            // B rows of the expert's windows: window w's half lives at 1 KiB... (w * 2048 B) in each CTA
-            const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
-            mma2_ts(dd, a0, bd, id, f0);
+            if (seg_par < 0 || (q & 1) == seg_par) {
+              tq = clock64();
+              mbar_wait_cluster(&S.afull[aslot], aph);
+              prof[3] += clock64() - tq;
+              tq = clock64();
+              tc_fence_after();
+              const int win0 = S.segs[q].win0;
+              const uint32_t id = idesc_bf16_m256(S.segs[q].winN);
+              const uint32_t dd = d_base + (uint32_t)(NP + win0);
+              const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
+              // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
+              const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
+              mma2_ts(dd, a0, bd, id, f0);
 #pragma unroll
-            for (int j = 1; j < 8; ++j) mma2_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
-            tc2_commit(&S.aempty[aslot]);
+              for (int j = 1; j < 8; ++j) mma2_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
+              tc2_commit(&S.aempty[aslot]);
+              prof[4] += clock64() - tq;
+              prof[7]++;
+            }
             if (++aslot == NA) { aslot = 0; aph ^= 1; }
-            prof[4] += clock64() - tq;
-            prof[7]++;
           }
           tc2_commit(&S.xempty[sx]);
           if (++sx == p.nx) { sx = 0; px ^= 1; }
@@ -657,10 +676,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           }
         }
       }
-      MESW_STAMP(3);
+      if (role == 0) MESW_STAMP(3);
       prof[6] = clock64() - tstart;
       if (p.tbuf)
-        for (int i = 0; i < 8; ++i) p.tbuf[4096 * 8 + (size_t)blockIdx.x * 16 + i] = prof[i];
+        for (int i = 0; i < 8; ++i) p.tbuf[4096 * 8 + (size_t)blockIdx.x * 16 + role * 8 + i] = prof[i];
     }
   } else if (warp < kEpiWarp0) {
     // ===================== dequant groups: own codes -> own TMEM A rows =====================
@@ -674,6 +693,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     int sc = 0;
     uint32_t pc = 0;
     int jpar = 0, jslot = 0, juse = 0;
+    long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long dstart = clock64();
+    long long dq;
     for (int pi = 0; pi < (p.n_seg > 0 ? po.np : 0); ++pi) {
       long long pa, pb;
       po.bounds(pi, pa, pb);
@@ -682,7 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           const int sg0 = ch * p.segs_per_chunk;
           const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
           const int off = (grp - jpar + kDqGroups) % kDqGroups;
+          dq = clock64();
           mbar_wait(&S.cfull[sc], pc);
+          dprof[0] += clock64() - dq;
           const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
           uint32_t cw[MJ][WPJ];
 #pragma unroll
@@ -709,7 +733,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               const int sj = jslot + (q - sg0);
               const int aslot = sj % NA;
               const int use = juse + sj / NA;
+              dq = clock64();
               if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
+              dprof[1] += clock64() - dq;
+              dq = clock64();
               const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
 #pragma unroll
               for (int kh = 0; kh < 2; ++kh) {
@@ -717,13 +744,17 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
                 dequant_chunk<DB>(&cw[jq][kh * (CHB / 4)], r);
                 tmem_st32(a0 + lane_addr + 32 * kh, r);
               }
+              dprof[2] += clock64() - dq;
+              dq = clock64();
               asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
               tc_fence_before();
               __syncwarp();
               if (lane == 0) {  // 4 warps of each CTA -> leader's afull (8 arrivals)
                 if (rank == 0) mbar_arrive(&S.afull[aslot]);
-                else mbar_arrive_cta(&S.afull[aslot], 0);
+                else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
               }
+              dprof[3] += clock64() - dq;
+              dprof[7]++;
             }
           }
           jpar = (jpar + (sg1 - sg0)) % kDqGroups;
@@ -732,6 +763,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
         }
       }
     }
+    dprof[6] = clock64() - dstart;
+    if (p.tbuf && quarter == 0 && lane == 0)
+      for (int i = 0; i < 8; ++i) p.tbuf[4096 * 24 + (size_t)blockIdx.x * 16 + grp * 8 + i] = dprof[i];
   } else {
     // ===================== epilogue warpgroup (own column group) =====================
     const int quarter = warp & 3;
@@ -807,6 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       if (!whole) {
         __threadfence();
         named_bar_sync(1, 128);
+        if (gtid == 0 && pi == po.np - 1) MESW_STAMP(1);
         // contributors to this column group: the pairs owning its first/last unit
         const long long first_u = (long long)cgp * p.n_ks, last_u = first_u + p.n_ks - 1;
         const int p_first = unit_owner(first_u, T2, (int)G2), p_last = unit_owner(last_u, T2, (int)G2);
@@ -815,10 +850,14 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           S.flag = (prev == p_last - p_first) ? 1 : 0;
         }
         named_bar_sync(1, 128);
+        if (gtid == 0 && pi == po.np - 1) MESW_STAMP(2);
         if (S.flag) {
+          long long ep[4] = {0, 0, 0, 0}, ec = clock64();
           __threadfence();
+          ep[3] = clock64() - ec;
           const size_t slot_floats = (size_t)2 * NP * kUnitN;
           for (int t0 = 0; t0 < NP; t0 += 16) {
+            ec = clock64();
             const int sg = S.tok2seg[t0];
             int cb0 = t0 / 2, cb1 = HP + t0 / 2, cd0 = -1, cd1 = -1;
             if (sg >= 0) {
@@ -830,20 +869,40 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             float vb[16], vd[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) vb[i] = vd[i] = 0.f;
-            for (int pp = p_first; pp <= p_last; ++pp) {
-              const long long pu0 = (long long)pp * T2 / G2;
-              const int s2 = 2 * (2 * pp + (int)rank) + ((int)(pu0 / p.n_ks) == cgp ? 0 : 1);
-              const float* src = p.ws + (size_t)s2 * slot_floats + mrow;
+            // all contributors' loads of this 16-row chunk are issued before any is used (one
+            // L2 round trip per chunk, not one per contributor); summed in fixed pair order
+            for (int pb = p_first; pb <= p_last; pb += kRedBatch) {
+              float lb[kRedBatch][16], ld[kRedBatch][16];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                vb[i] += __ldcg(src + (size_t)(cb0 + i) * kUnitN);
-                vb[8 + i] += __ldcg(src + (size_t)(cb1 + i) * kUnitN);
+              for (int b = 0; b < kRedBatch; ++b) {
+                const int pp = pb + b;
+                if (pp <= p_last) {
+                  const long long pu0 = (long long)pp * T2 / G2;
+                  const int s2 = 2 * (2 * pp + (int)rank) + ((int)(pu0 / p.n_ks) == cgp ? 0 : 1);
+                  const float* src = p.ws + (size_t)s2 * slot_floats + mrow;
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) {
+                    lb[b][i] = __ldcg(src + (size_t)(cb0 + i) * kUnitN);
+                    lb[b][8 + i] = __ldcg(src + (size_t)(cb1 + i) * kUnitN);
+                  }
+                  if (cd0 >= 0) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                      ld[b][i] = __ldcg(src + (size_t)(cd0 + i) * kUnitN);
+                      ld[b][8 + i] = __ldcg(src + (size_t)(cd1 + i) * kUnitN);
+                    }
+                  }
+                }
               }
-              if (cd0 >= 0) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  vd[i] += __ldcg(src + (size_t)(cd0 + i) * kUnitN);
-                  vd[8 + i] += __ldcg(src + (size_t)(cd1 + i) * kUnitN);
+              for (int b = 0; b < kRedBatch; ++b) {
+                if (pb + b <= p_last) {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) vb[i] += lb[b][i];
+                  if (cd0 >= 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) vd[i] += ld[b][i];
+                  }
                 }
               }
             }
@@ -851,14 +910,24 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
 #pragma unroll
               for (int i = 0; i < 16; ++i) vb[i] = 0.f;
             }
+            float vsum = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vsum += vb[i] + vd[i];
+            if (vsum == 12345.f) S.flag = 2;  // forces the partial loads to complete here (timing)
+            ep[0] += clock64() - ec; ec = clock64();
             epi_store16(p, S, cg, mrow, t0, vb, vd, fast, pre);
+            ep[1] += clock64() - ec; ec = clock64();
             if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
+            ep[2] += clock64() - ec;
           }
+          if (gtid == 0 && pi == po.np - 1) MESW_STAMP(4);
+          if (gtid == 0 && pi == po.np - 1 && p.tbuf)
+            for (int i = 0; i < 4; ++i) p.tbuf[4096 * 40 + (size_t)blockIdx.x * 16 + i] = ep[i];
           if (gtid == 0) p.counters[cg] = 0;  // self-reset for the next launch
         }
       }
       named_bar_sync(1, 128);  // xsal / flag reuse by the next piece
-      if (gtid == 0) MESW_STAMP(pi == po.np - 1 ? 7 : 4);
+      if (gtid == 0 && pi == po.np - 1) MESW_STAMP(7);
     }
   }
 
@@ -908,7 +977,7 @@ static unsigned long long* g_tbuf = nullptr;
 // Debug: copy the last MESW_TIMING launch's per-CTA globaltimer stamps (8 per CTA).
 extern "C" int mesw_debug_timing_copy(unsigned long long* h_out, int n_ctas) {
   if (!g_tbuf) return mesw_fail(MESW_ERR_VALUE, "no timing buffer (set MESW_TIMING)");
-  cudaError_t e = cudaMemcpy(h_out, g_tbuf, (size_t)16 * 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpy(h_out, g_tbuf, (size_t)56 * 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? MESW_OK : mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
 }
 
@@ -964,7 +1033,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
     const char* e = getenv("MESW_DBG");
     p.dbg = e ? atoi(e) : 0;
     if (getenv("MESW_TIMING")) {
-      if (!g_tbuf) cudaMalloc(&g_tbuf, 16 * 4096 * sizeof(unsigned long long));
+      if (!g_tbuf) cudaMalloc(&g_tbuf, 56 * 4096 * sizeof(unsigned long long)); cudaMemset(g_tbuf, 0, 56 * 4096 * 8);
       p.tbuf = g_tbuf;
     }
   }
@@ -984,7 +1053,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   p.cbytes = p.segs_per_chunk * CB;
   const size_t budget = 232448 - ring_offset();
   // ring depths: prefer (x 3, codes 3, weights >= 3); shrink x/codes first when rows are many
-  p.nx = 3;
+  p.nx = getenv("MESW_NX") ? atoi(getenv("MESW_NX")) : 3;
   p.nc = p.n_chunks > 0 ? 3 : 0;
   for (;;) {
     const size_t used = (size_t)p.nx * p.xbytes + (size_t)p.nc * p.cbytes + 1024;
@@ -1015,6 +1084,11 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   if (na < kDqGroups) return mesw_fail(MESW_ERR_UNSUPPORTED, "tensor memory: too many rows for the A ring");
   p.n_aslots = na;
   p.a_col0 = kTmemCols - na * kAColsPerSlot;
+  {
+    int iss = (p.w ? 1 : 0) + p.n_seg;
+    if (getenv("MESW_ISS")) iss = std::min(iss, atoi(getenv("MESW_ISS")));
+    p.n_iss = iss < kMaxIssuers ? (iss < 1 ? 1 : iss) : kMaxIssuers;
+  }
 
   cudaStream_t s = (cudaStream_t)stream;
   switch (db) {

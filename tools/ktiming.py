@@ -21,12 +21,13 @@ torch.cuda.synchronize()
 plan(); torch.cuda.synchronize()
 G = min(148, (n // 128) * (m // 128))
 G -= G % 2
-buf = np.zeros(16 * 4096, np.uint64)
+buf = np.zeros(56 * 4096, np.uint64)
 _lib.check(L.mesw_debug_timing_copy(buf.ctypes.data, G))
 t = buf[:G * 8].reshape(G, 8).astype(np.int64)
 prof = buf[4096 * 8:4096 * 8 + G * 16].reshape(G, 2, 8).astype(np.int64)
+dprof = buf[4096 * 24:4096 * 24 + G * 16].reshape(G, 2, 8).astype(np.int64)
 t0 = t[:, 0].min()
-names = ["start", "prod_done", "mma_unit0", "mma_done", "epi_first", "last_accfull", "last_tmem", "last_end"]
+names = ["start", "ws_fenced", "flag_known", "mma_done", "red_done", "last_accfull", "last_tmem", "last_end"]
 print(f"m={m} n={n} E={E} rows={rows}  (us from first CTA start)")
 for i, nm in enumerate(names):
     v = (t[:, i] - t0) / 1e3
@@ -35,7 +36,13 @@ for i, nm in enumerate(names):
         print(f"  {nm:12s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f}")
 
 pm = ["wait_x", "wait_w", "base_issue", "wait_afull", "delta_issue", "wait_accempty", "total", "jobs"]
-pd = ["wait_cfull", "wait_aempty", "dequant+st", "-", "-", "-", "total", "jobs"]
+pd = ["wait_cfull", "wait_aempty", "dequant+st", "wait_st+arrive", "-", "-", "total", "jobs"]
 lead = prof[0::2, 0, :]
 print("  mma   ", " ".join(f"{pm[i]}={np.median(lead[:, i]):.0f}" for i in range(8)))
-print("  deq0  ", " ".join(f"{pd[i]}={np.median(prof[:, 1, i]):.0f}" for i in range(8) if pd[i] != "-"))
+print("  mma2  ", " ".join(f"{pm[i]}={np.median(prof[0::2, 1, i]):.0f}" for i in range(8)))
+for g in range(2):
+    for r, nm in ((0, "lead"), (1, "peer")):
+        print(f"  deq{g} {nm}", " ".join(f"{pd[i]}={np.median(dprof[r::2, g, i]):.0f}" for i in range(8) if pd[i] != "-"))
+eprof = buf[4096 * 40:4096 * 40 + G * 16].reshape(G, 16).astype(np.int64)
+sel = eprof[:, 0] > 0
+print("  red (last arrivers, cycles):", " ".join(f"{n}={np.median(eprof[sel, i]):.0f}" for i, n in enumerate(["loads", "store", "prefetch", "fence"])), f"n={sel.sum()}")

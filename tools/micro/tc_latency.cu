@@ -21,7 +21,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
   asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
 }
 
-__global__ void bench(int M, int N, int R, unsigned long long* out, int ts) {
+__global__ void bench(int M, int N, int R, unsigned long long* out, int ts, int nis) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t tb;
   __shared__ __align__(8) uint64_t bar;
@@ -31,7 +31,7 @@ __global__ void bench(int M, int N, int R, unsigned long long* out, int ts) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(nis));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3F803F80u;
@@ -39,14 +39,16 @@ __global__ void bench(int M, int N, int R, unsigned long long* out, int ts) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t t = tb;
-  if (warp == 1) {
-    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 65536);
+  if (warp >= 1 && warp <= nis) {
+    const uint32_t a = smem_u32(sm) + (warp - 1) * 16384, b = smem_u32(sm + 65536) + (warp - 1) * 16384;
     const uint32_t id = idesc(M, N);
     const uint64_t da = sdesc(a), db = sdesc(b);
     unsigned long long g0, g1;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g0));
     long long c0 = clock64();
-    if (threadIdx.x == 32) {
+    const uint32_t t0 = t;
+    if ((threadIdx.x & 31) == 0) {
+      const uint32_t t = t0 + (warp - 1) * (N <= 128 ? 128 : 256);
       for (int i = 0; i < R; i += 8) {
         if (ts == 1) {
 #pragma unroll
@@ -73,6 +75,7 @@ __global__ void bench(int M, int N, int R, unsigned long long* out, int ts) {
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     }
+
     __syncwarp();
     long long c1 = clock64();
     asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra W;\n}\n" ::"r"(smem_u32(&bar)));
@@ -89,24 +92,23 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 32);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
-  const int R = 4096;  // multiple of 16
-  const char* nm[] = {"SS", "TS", "SS-alt8", "SS/TS-alt8", "SS-alt1"};
-  for (int swz = 0; swz < 2; ++swz) {
-  cudaMemcpyToSymbol(g_swz, &swz, sizeof(int));
-  printf("swizzle %d\n", swz);
+  const int R = 4096;
+  int zero = 0;
+  cudaMemcpyToSymbol(g_swz, &zero, sizeof(int));
+  const char* nm[] = {"SS", "TS"};
   for (int ts = 0; ts < 2; ++ts)
-    for (int M : {128})
-      for (int N : {16, 48}) {
-        bench<<<1, 128, 131072>>>(M, N, R, d, ts);
-        printf("%-11s ", nm[ts]);
-        unsigned long long h[3];
-        cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
-        double macs = (double)M * N * 16;
-        printf("M=%3d N=%3d: issue %6.1f cyc/mma, complete %6.1f cyc/mma, %6.1f ns/mma, %7.0f MAC/cyc, clk %.2f GHz\n",
-               M, N, (double)h[0] / R, (double)h[1] / R, (double)h[2] / R, macs / ((double)h[1] / R),
-               (double)h[1] / h[2]);
-      }
-  }
+    for (int nis : {1, 2})
+      for (int M : {64, 128})
+        for (int N : {16, 32, 64, 128, 256}) {
+          if (nis == 2 && N > 128) continue;
+          if (ts == 1 && N > 128) continue;
+          bench<<<1, 128, 131072>>>(M, N, R, d, ts, nis);
+          unsigned long long h[3];
+          cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+          double macs = (double)M * N * 16 * nis;
+          printf("%s issuers %d M=%3d N=%3d: issue %6.1f cyc/mma, complete %6.1f cyc/mma (per issuer), %7.0f MAC/cyc total\n",
+                 nm[ts], nis, M, N, (double)h[0] / R, (double)h[1] / R, macs / ((double)h[1] / R));
+        }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
