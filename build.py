@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
+if os.environ.get("MESW_PROFILE"):  # role-loop cycle counters for tools/ktiming.py (rebuild with --force)
+    FLAGS.append("-DMESW_PROFILE")
 
 
 def sources():

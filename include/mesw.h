@@ -58,6 +58,11 @@ int mesw_abi_version(void);
 const char* mesw_last_error(void);
 /* Number of SMs of the current device (grid sizing), or -1. */
 int mesw_device_sm_count(void);
+/* Programmatic dependent launch for every kernel of this library (default on): a
+ * launch may begin -- prologue, weight / code prefetch -- while the previous kernel
+ * in the stream drains; each kernel waits (griddepcontrol.wait) before touching
+ * data a previous kernel produces or consumes.  Returns the previous setting.   */
+int mesw_set_pdl(int enable);
 
 /* --------------------------------------------- MESW container (host side)
  * Replaces compress.deserialize_artifact (compress.py:513-549): validates the

@@ -44,6 +44,7 @@ _SIGNATURES = [
     ("mesw_abi_version", C.c_int, []),
     ("mesw_last_error", C.c_char_p, []),
     ("mesw_device_sm_count", C.c_int, []),
+    ("mesw_set_pdl", C.c_int, [C.c_int]),
     ("mesw_parse_header", C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]),
     ("mesw_parse_layers", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.POINTER(LayerView)]),
     ("mesw_packed_nbytes", C.c_uint64, [C.c_uint32, C.c_uint32, C.c_uint32]),

@@ -30,6 +30,14 @@ int mesw_check_launch(const char* what) {
 
 extern "C" int mesw_abi_version(void) { return 1; }
 
+static int g_pdl = 1;
+int mesw_pdl_enabled() { return g_pdl; }
+extern "C" int mesw_set_pdl(int enable) {
+  const int prev = g_pdl;
+  g_pdl = enable ? 1 : 0;
+  return prev;
+}
+
 extern "C" const char* mesw_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" int mesw_device_sm_count(void) {

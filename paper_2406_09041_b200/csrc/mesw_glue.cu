@@ -59,6 +59,8 @@ __device__ __forceinline__ float block_max(float v, float* red) {
 
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __restrict__ table,
                              int H, uint16_t* __restrict__ out, int ld_out) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   const int b = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)ids[b] * H);
   uint4* dst = reinterpret_cast<uint4*>(out + (size_t)b * ld_out);
@@ -72,6 +74,8 @@ constexpr int kNormMaxVec = 4;  // up to 256 * 4 * 8 = 8192 channels
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* __restrict__ x, int ldx,
                                                                const uint16_t* __restrict__ w, int H, float eps,
                                                                uint16_t* __restrict__ y, int ldy, int ynp) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   __shared__ float red[32];
   const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)blockIdx.x * ldx);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
@@ -114,6 +118,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
 __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int ld_qkv, const int32_t* __restrict__ pos,
                                    int n_heads, int n_kv, int D, float theta,
                                    uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int ctx_max) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   const int b = blockIdx.x, h = blockIdx.y, i = threadIdx.x, half = D / 2;
   const int p = pos[b];
   const float inv = powf(theta, -2.0f * (float)i / (float)D);
@@ -157,6 +163,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(
     const uint16_t* __restrict__ q, int ld_q, const uint16_t* __restrict__ kc, const uint16_t* __restrict__ vc,
     const int32_t* __restrict__ len, int n_kv, int ctx_max, float scale, uint16_t* __restrict__ out, int ld_out,
     int out_np) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   constexpr int D = 128;
   extern __shared__ __align__(16) uint8_t smraw[];
   uint16_t* Ks = reinterpret_cast<uint16_t*>(smraw);                  // [L][136]
@@ -262,6 +270,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(
 // out = silu(gate) * up, gate/up halves of a [B][2I] row.
 __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int ld_gu, int I, uint16_t* __restrict__ out,
                               int ld_out, int out_np) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   const int b = blockIdx.y;
   const uint16_t* r = gu + (size_t)b * ld_gu;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2; i < I; i += gridDim.x * blockDim.x * 2) {
@@ -277,6 +287,8 @@ __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int ld_gu, int I,
 // argmax over a row with ties to the lowest index (np.argmax); f32 or bf16 logits.
 __global__ void argmax_kernel(const void* __restrict__ logits, int is_bf16, int V, int ld,
                               int32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   __shared__ float bv[32];
   __shared__ int bi[32];
   const int b = blockIdx.x;
@@ -313,6 +325,8 @@ __global__ void argmax_kernel(const void* __restrict__ logits, int is_bf16, int 
 // Row-major -> canonical (one thread per 16-byte chunk of 8 k); zero padding.
 __global__ void pack_x_kernel(const uint16_t* __restrict__ x, int B, int m, int ldx, uint16_t* __restrict__ xc,
                               int NP, int n_ks) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)n_ks * NP * 16;
   if (tid >= total) return;
@@ -337,6 +351,8 @@ __global__ void pack_x_kernel(const uint16_t* __restrict__ x, int B, int m, int 
 
 __global__ void unpack_x_kernel(const uint16_t* __restrict__ xc, int B, int m, int NP, uint16_t* __restrict__ y,
                                 int ldy) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)B * m) return;
   const int t = (int)(tid / m), k = (int)(tid % m);
@@ -347,6 +363,8 @@ __global__ void unpack_x_kernel(const uint16_t* __restrict__ xc, int B, int m, i
 // reaches the end of its cache window wraps back to `wrap_to` (bench steady state).
 __global__ void advance_kernel(int32_t* __restrict__ pos, int32_t* __restrict__ len, int B, int ctx_max,
                                int wrap_to) {
+  pdl_trigger();
+  pdl_wait();  // inputs may come from the previous kernel in the stream
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int p = pos[b] + 1;
@@ -362,14 +380,14 @@ using namespace mesw;
 extern "C" int mesw_advance_positions(int32_t* d_pos, int32_t* d_len, int B, int ctx_max, int wrap_to,
                                       void* stream) {
   if (B <= 0 || wrap_to < 0 || wrap_to >= ctx_max) return mesw_fail(MESW_ERR_VALUE, "advance: bad args");
-  advance_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(d_pos, d_len, B, ctx_max, wrap_to);
+  mesw_launch(advance_kernel, dim3((B + 127) / 128), dim3(128), 0, (cudaStream_t)stream, d_pos, d_len, B, ctx_max, wrap_to);
   return mesw_check_launch("advance_positions");
 }
 
 extern "C" int mesw_embed(const int32_t* d_ids, int B, const uint16_t* d_table, int H, uint16_t* d_out,
                           int ld_out, void* stream) {
   if (B <= 0 || H % 8) return mesw_fail(MESW_ERR_VALUE, "embed: H must be a multiple of 8");
-  embed_kernel<<<B, 128, 0, (cudaStream_t)stream>>>(d_ids, d_table, H, d_out, ld_out);
+  mesw_launch(embed_kernel, dim3(B), dim3(128), 0, (cudaStream_t)stream, d_ids, d_table, H, d_out, ld_out);
   return mesw_check_launch("embed");
 }
 
@@ -378,7 +396,7 @@ extern "C" int mesw_rmsnorm(const uint16_t* d_x, int ldx, const uint16_t* d_w, i
   if (B <= 0 || H % 8 || H > kNormThreads * kNormMaxVec * 8 || ldx % 8 || ldy % 8)
     return mesw_fail(MESW_ERR_VALUE, "rmsnorm: H and strides must be multiples of 8, H <= 8192");
   if (y_np > 0 && (y_np % 16 || y_np < B)) return mesw_fail(MESW_ERR_VALUE, "rmsnorm: canonical rows must be >= B, multiple of 16");
-  rmsnorm_kernel<<<B, kNormThreads, 0, (cudaStream_t)stream>>>(d_x, ldx, d_w, H, eps, d_y, ldy, y_np);
+  mesw_launch(rmsnorm_kernel, dim3(B), dim3(kNormThreads), 0, (cudaStream_t)stream, d_x, ldx, d_w, H, eps, d_y, ldy, y_np);
   return mesw_check_launch("rmsnorm");
 }
 
@@ -387,9 +405,7 @@ extern "C" int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_po
                                 int ctx_max, void* stream) {
   if (B <= 0 || head_dim % 2 || head_dim > 2048) return mesw_fail(MESW_ERR_VALUE, "rope: bad shape");
   dim3 grid(B, n_heads + n_kv);
-  rope_append_kernel<<<grid, head_dim / 2, 0, (cudaStream_t)stream>>>(d_qkv, ld_qkv, d_pos, n_heads, n_kv,
-                                                                      head_dim, theta, d_kcache, d_vcache,
-                                                                      ctx_max);
+  mesw_launch(rope_append_kernel, dim3(grid), dim3(head_dim / 2), 0, (cudaStream_t)stream, d_qkv, ld_qkv, d_pos, n_heads, n_kv, head_dim, theta, d_kcache, d_vcache, ctx_max);
   return mesw_check_launch("rope_append");
 }
 
@@ -415,8 +431,8 @@ extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16
       if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));                     \
       cfg = true;                                                                                       \
     }                                                                                                   \
-    attn_decode_kernel<GG><<<grid, kAttnThreads, smem, s>>>(d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, \
-                                                            ctx_max, scale, d_out, ld_out, out_np);     \
+    mesw_launch(attn_decode_kernel<GG>, dim3(grid), dim3(kAttnThreads), smem, s, d_q, ld_q, d_kcache,         \
+                d_vcache, d_len, n_kv, ctx_max, scale, d_out, ld_out, out_np);                             \
     break;                                                                                              \
   }
   switch (G) {
@@ -435,14 +451,14 @@ extern "C" int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16
                            int out_np, void* stream) {
   if (B <= 0 || I % 2) return mesw_fail(MESW_ERR_VALUE, "swiglu: bad shape");
   dim3 grid((I / 2 + 255) / 256 < 64 ? (I / 2 + 255) / 256 : 64, B);
-  swiglu_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_gu, ld_gu, I, d_out, ld_out, out_np);
+  mesw_launch(swiglu_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, d_gu, ld_gu, I, d_out, ld_out, out_np);
   return mesw_check_launch("swiglu");
 }
 
 extern "C" int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int ld, int32_t* d_out,
                            void* stream) {
   if (B <= 0 || V <= 0) return mesw_fail(MESW_ERR_VALUE, "argmax: bad shape");
-  argmax_kernel<<<B, 1024, 0, (cudaStream_t)stream>>>(d_logits, is_bf16, V, ld, d_out);
+  mesw_launch(argmax_kernel, dim3(B), dim3(1024), 0, (cudaStream_t)stream, d_logits, is_bf16, V, ld, d_out);
   return mesw_check_launch("argmax");
 }
 
@@ -450,7 +466,7 @@ extern "C" int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t*
   if (B <= 0 || m <= 0 || ldx < m) return mesw_fail(MESW_ERR_VALUE, "pack_x: bad shape");
   const int NP = (B + 15) & ~15, n_ks = (m + 127) / 128;
   const long long total = (long long)n_ks * NP * 16;
-  pack_x_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_x, B, m, ldx, d_xc, NP, n_ks);
+  mesw_launch(pack_x_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, d_x, B, m, ldx, d_xc, NP, n_ks);
   return mesw_check_launch("pack_x");
 }
 
@@ -458,6 +474,6 @@ extern "C" int mesw_unpack_x(const uint16_t* d_xc, int B, int m, uint16_t* d_y, 
   if (B <= 0 || m <= 0 || ldy < m) return mesw_fail(MESW_ERR_VALUE, "unpack_x: bad shape");
   const int NP = (B + 15) & ~15;
   const long long total = (long long)B * m;
-  unpack_x_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_xc, B, m, NP, d_y, ldy);
+  mesw_launch(unpack_x_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, d_xc, B, m, NP, d_y, ldy);
   return mesw_check_launch("unpack_x");
 }

@@ -32,20 +32,20 @@
 
 namespace mesw {
 
-constexpr int kDqGroups = 2;  // dequant warpgroups: group g expands k-half g of every job
-// warp roles: 0 weight-tile producer, 1-2 MMA issuers, 3 activation + code producer, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
-constexpr int kWProdWarp = 0, kMmaWarp = 1, kMma2Warp = 2, kCProdWarp = 3;
-constexpr int kMaxIssuers = 2;
+constexpr int kDqGroups = 2;  // dequant warpgroups: group (k % 2) expands issuer stream job k
+// warp roles: 0 producer (codes, weight tiles, activations), 1-3 MMA issuers, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
+constexpr int kProdWarp = 0, kMmaWarp = 1;
+constexpr int kMaxIssuers = 3;  // warps 1..3
 constexpr int kDqWarp0 = 4, kEpiWarp0 = kDqWarp0 + 4 * kDqGroups;
 constexpr int kThreads = (kEpiWarp0 + 4) * 32;  // 16 warps
 constexpr int kTmemCols = 512;
-constexpr int kMaxASlots = 6;
-constexpr int kAColsPerSlot = 64;
+constexpr int kMaxASlots = 8;
+constexpr int kAColsPerSlot = 64;  // one job's A tile (128 x 128 bf16) per slot
 constexpr int kMaxRows = 192;  // padded token rows per launch (TMEM: 2 * rows <= 384)
 constexpr int kMaxStages = 8;
+constexpr int kMaxCStages = 16;
 constexpr int kXRowGroupBytes = 2048;  // 8 token rows x 16 k-chunks x 16 B
 constexpr int kSalFast = 16;           // salient rows per column group handled from smem
-constexpr int kRedBatch = 1;           // stream-K partials loaded per L2 round trip
 
 // Element index of x[t][k] in the canonical activation layout (see mesw.h): per 128-wide
 // k-step, two halves h = (t/8)%2 (rows 0-7 / 8-15 of every 16-row window), each a
@@ -90,6 +90,12 @@ struct LinearParams {
   int nc, co, cbytes, segs_per_chunk, n_chunks;
   // tensor memory: n_acc accumulator buffers of 2*NP columns, A ring from a_col0
   int n_acc, n_aslots, a_col0;
+  // A ring split per MMA issuer: issuer i owns slots [a_base[i], a_base[i] + a_na[i]) (a_na even)
+  // and consumes its jobs in order; dequant group (k % 2) writes issuer i's k-th job.  Every
+  // slot is therefore written by one group and read by one issuer, in sequence, so the
+  // mbarrier parity waits on it can never alias a phase two steps away.
+  int a_base[3], a_na[3];
+  int ring_bytes;  // dynamic shared memory past the Smem header
   int n_iss;  // MMA issuer threads (a tcgen05.mma stream runs ~60-85 cycles/instr per issuer)
   unsigned long long* tbuf;  // MESW_TIMING: per-CTA globaltimer stamps
   int dbg;  // perf experiments: bit0 skip dequant math, bit1 skip delta MMAs, bit2 skip tcgen05.st
@@ -98,11 +104,13 @@ struct LinearParams {
 struct Smem {
   uint64_t xfull[kMaxStages], xempty[kMaxStages];
   uint64_t wfull[kMaxStages], wempty[kMaxStages];
-  uint64_t cfull[kMaxStages], cempty[kMaxStages];
+  uint64_t cfull[kMaxCStages], cempty[kMaxCStages];
   uint64_t afull[kMaxASlots], aempty[kMaxASlots];
   uint64_t accfull[2], accempty[2];
+  uint64_t finbar;  // final-piece partials staged by bulk copy
   uint32_t tmem_base;
   int flag;
+  struct { int on, cg, cgp, p_first, p_last, fast; } fin;  // final-piece reduction hand-off
   int tok2seg[kMaxRows];
   SegDesc segs[MESW_MAX_SEGMENTS];
   int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
@@ -163,6 +171,12 @@ __device__ __forceinline__ void tc2_commit(uint64_t* bar) {
           smem_u32(bar)),
       "h"((uint16_t)3)
       : "memory");
+}
+
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* ptr, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(ptr), "r"(v) : "memory");
+  return old;
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -454,11 +468,87 @@ __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S
   }
 }
 
+// Stream-K reduction + epilogue of one 16-row chunk of column group cg (thread owns
+// column m): the contributors' partials are summed in fixed pair order (bit-identical for
+// any launch geometry with the same row count), then stored through epi_store16.  The
+// epilogue operands are fetched together with the partials: one L2 round trip per chunk.
+// stage != nullptr: the contributors' slots were bulk-copied to shared memory (final piece).
+__device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& S, int cg, int cgp, int rank, int m,
+                                          int t0, int p_first, int p_last, bool fast, const EpiPre& pre,
+                                          const float* stage) {
+  const int NP = p.NP, HP = NP / 2;
+  const long long T2 = p.T, G2 = p.G / 2;
+  const int sg = S.tok2seg[t0];
+  int cb0 = t0 / 2, cb1 = HP + t0 / 2, cd0 = -1, cd1 = -1;
+  if (sg >= 0) {
+    const SegDesc& sd = S.segs[sg];
+    const int dw = (t0 - sd.win0) / 2;
+    cd0 = NP + sd.win0 + dw;
+    cd1 = NP + sd.win0 + sd.winN / 2 + dw;
+  }
+  const size_t slot_floats = (size_t)2 * NP * kUnitN;
+  float vb[16], vd[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) vb[i] = vd[i] = 0.f;
+  for (int pp = p_first; pp <= p_last; ++pp) {
+    float lb[16], ld[16];
+    if (stage) {
+      const float* src = stage + (size_t)(pp - p_first) * slot_floats + m;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        lb[i] = src[(size_t)(cb0 + i) * kUnitN];
+        lb[8 + i] = src[(size_t)(cb1 + i) * kUnitN];
+      }
+      if (cd0 >= 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ld[i] = src[(size_t)(cd0 + i) * kUnitN];
+          ld[8 + i] = src[(size_t)(cd1 + i) * kUnitN];
+        }
+      }
+    } else {
+      const long long pu0 = (long long)pp * T2 / G2;
+      const int s2 = 2 * (2 * pp + rank) + ((int)(pu0 / p.n_ks) == cgp ? 0 : 1);
+      const float* src = p.ws + (size_t)s2 * slot_floats + m;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        lb[i] = __ldcg(src + (size_t)(cb0 + i) * kUnitN);
+        lb[8 + i] = __ldcg(src + (size_t)(cb1 + i) * kUnitN);
+      }
+      if (cd0 >= 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ld[i] = __ldcg(src + (size_t)(cd0 + i) * kUnitN);
+          ld[8 + i] = __ldcg(src + (size_t)(cd1 + i) * kUnitN);
+        }
+      }
+    }
+    if (cd0 >= 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) vd[i] += ld[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) vb[i] += lb[i];
+  }
+  if (p.w == nullptr) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) vb[i] = 0.f;
+  }
+  epi_store16(p, S, cg, m, t0, vb, vd, fast, pre);
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Cycle-count profiling of the role loops (tools/ktiming.py): compiled in only with
+// -DMESW_PROFILE (MESW_PROFILE=1 python build.py --force); zero cost otherwise.
+#ifdef MESW_PROFILE
+#define MESW_PROF(...) __VA_ARGS__
+#else
+#define MESW_PROF(...)
+#endif
 #define MESW_STAMP(i) \
   do { if (p.tbuf) p.tbuf[(size_t)blockIdx.x * 8 + (i)] = gtimer(); } while (0)
 
@@ -494,6 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     for (int i = 0; i < p.nc; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 128 * kDqGroups); }
     for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 8); mbar_init(&S.aempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], p.n_iss); mbar_init(&S.accempty[i], 8); }
+    mbar_init(&S.finbar, 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -502,6 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   for (int i = threadIdx.x; i < kMaxRows; i += kThreads) S.tok2seg[i] = -1;
+  if (threadIdx.x == 0) S.fin.on = 0;
   __syncthreads();
   for (int q = threadIdx.x; q < p.n_seg; q += kThreads) {
     const mesw_expert_dev e = p.table[p.seg_slot[q]];
@@ -525,51 +617,69 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   const uint32_t tbase = S.tmem_base;
   const bool has_w = p.w != nullptr;
   if (threadIdx.x == 0) MESW_STAMP(0);
+  pdl_trigger();
 
-  if (warp == kWProdWarp || warp == kCProdWarp) {
-    // ===================== producers (own column group / own x half) =====================
-    uint64_t evict_first;  // weights / codes are streamed once: do not let them evict partials
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
-    int st = 0, sx = 0;
-    uint32_t ph = 0, px = 0;
-    bool first = true, xfirst = true;
-    for (int pi = 0; pi < po.np; ++pi) {
-      long long pa, pb;
-      po.bounds(pi, pa, pb);
-      const int cgp = po.cg_of(pi);
-      const int cg = 2 * cgp + (int)rank;
-      for (long long u = pa; u < pb; ++u) {
-        const int ks = (int)(u - (long long)cgp * p.n_ks);
+  if (warp == kProdWarp) {
+    // ===================== producer (own column group / own x half), one thread =====================
+    // per unit: code chunks (the dequant groups run ahead), weight tile, activation half-tile
+    if (lane == 0) {
+      uint64_t evict_first;  // weights / codes are streamed once: do not let them evict partials
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
+      int sw = 0, sx = 0, sc = 0;
+      uint32_t pw = 0, px = 0, pc = 0;
+      bool wfirst = true, xfirst = true, cfirst = true;
+      // Codes and weight tiles are static: the first ring's worth is requested before
+      // waiting for the previous kernel (PDL), activations only after it completed.
+      int n_pre = 0;
+      auto issue_static = [&](int cg, int ks) {
         const long long unit = (long long)cg * p.n_ks + ks;  // this CTA's unit
-        if (warp == kWProdWarp) {
-          if (lane == 0 && has_w) {
-            if (!first) mbar_wait(&S.wempty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&S.wfull[st], kUnitWBytes);
-            bulk_g2s_hint(ring + p.wo + (size_t)st * kUnitWBytes, p.w + (size_t)unit * kUnitWBytes, kUnitWBytes,
-                          &S.wfull[st], evict_first);
-            if (++st == p.nw) { st = 0; ph ^= 1; first = false; }
-          }
-        } else if (lane == 0) {
-          // activation half-tile, then this unit's code chunks (one thread: no divergent spinning)
+        for (int ch = 0; ch < p.n_chunks; ++ch) {
+          const int sg0 = ch * p.segs_per_chunk;
+          const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
+          if (!cfirst) mbar_wait(&S.cempty[sc], pc ^ 1);
+          mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
+          for (int q = sg0; q < sg1; ++q)
+            bulk_g2s_hint(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB,
+                          S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[sc], evict_first);
+          if (++sc == p.nc) { sc = 0; pc ^= 1; cfirst = false; }
+        }
+        if (has_w) {
+          if (!wfirst) mbar_wait(&S.wempty[sw], pw ^ 1);
+          mbar_arrive_expect_tx(&S.wfull[sw], kUnitWBytes);
+          bulk_g2s_hint(ring + p.wo + (size_t)sw * kUnitWBytes, p.w + (size_t)unit * kUnitWBytes, kUnitWBytes,
+                        &S.wfull[sw], evict_first);
+          if (++sw == p.nw) { sw = 0; pw ^= 1; wfirst = false; }
+        }
+      };
+      {
+        const int D = min(p.nx, p.nc > 0 ? p.nc / max(p.n_chunks, 1) : p.nx);
+        for (int pi = 0; pi < po.np && n_pre < D; ++pi) {
+          long long pa, pb;
+          po.bounds(pi, pa, pb);
+          const int cgp = po.cg_of(pi);
+          for (long long u = pa; u < pb && n_pre < D; ++u, ++n_pre)
+            issue_static(2 * cgp + (int)rank, (int)(u - (long long)cgp * p.n_ks));
+        }
+      }
+      pdl_wait();
+      int idx = 0;
+      for (int pi = 0; pi < po.np; ++pi) {
+        long long pa, pb;
+        po.bounds(pi, pa, pb);
+        const int cgp = po.cg_of(pi);
+        const int cg = 2 * cgp + (int)rank;
+        for (long long u = pa; u < pb; ++u, ++idx) {
+          const int ks = (int)(u - (long long)cgp * p.n_ks);
+          if (idx >= n_pre) issue_static(cg, ks);
           if (!xfirst) mbar_wait(&S.xempty[sx], px ^ 1);
           mbar_arrive_expect_tx(&S.xfull[sx], (uint32_t)p.xbytes);
           bulk_g2s(ring + p.xo + (size_t)sx * p.xbytes, p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK,
                    p.xbytes, &S.xfull[sx]);
           if (++sx == p.nx) { sx = 0; px ^= 1; xfirst = false; }
-          for (int ch = 0; ch < p.n_chunks; ++ch) {
-            const int sg0 = ch * p.segs_per_chunk;
-            const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-            if (!first) mbar_wait(&S.cempty[st], ph ^ 1);
-            mbar_arrive_expect_tx(&S.cfull[st], (uint32_t)(sg1 - sg0) * CB);
-            for (int q = sg0; q < sg1; ++q)
-              bulk_g2s_hint(ring + p.co + (size_t)st * p.cbytes + (size_t)(q - sg0) * CB,
-                            S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[st], evict_first);
-            if (++st == p.nc) { st = 0; ph ^= 1; first = false; }
-          }
         }
       }
     }
-  } else if (warp == kMmaWarp || warp == kMma2Warp) {
+  } else if (warp >= kMmaWarp && warp < kMmaWarp + kMaxIssuers) {
     const int role = warp - kMmaWarp;
     if (rank != 0) {
       // ===================== peer: relay "x / weight tile landed" to the leader =====================
@@ -593,49 +703,50 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       }
     } else if (lane == 0 && role < p.n_iss) {
       // ===================== leader: issue the pair's MMAs =====================
-      // Issuer 0: base tile + odd segments; issuer 1: even segments (one issuer: everything).
-      // Each segment's delta accumulator is owned by exactly one issuer, so the k-ordered
-      // accumulate chain of every TMEM column range stays in one thread's issue order.
+      // MMA streams (the base tile, then one per segment) are dealt round-robin to the
+      // issuers: stream s -> issuer s % n_iss.  Each accumulator range is owned by exactly
+      // one issuer, so its k-ordered accumulate chain stays in one thread's issue order.
+      const int s0 = has_w ? 1 : 0;  // stream index of segment 0
       const bool do_base = has_w && role == 0;
-      const int seg_par = p.n_iss == 1 ? -1 : (role ^ 1);
       const uint64_t xdesc0 = smem_desc(smem_u32(ring + p.xo));
       const uint64_t wdesc0 = smem_desc(smem_u32(ring + p.wo));
       const uint32_t xstride = (uint32_t)p.xbytes >> 4, wstride = kUnitWBytes >> 4;
       const uint32_t id_base = idesc_bf16_m256(NP);
-      const int NA = p.n_aslots;
+      const int na_own = p.a_na[role], abase_own = p.a_base[role];
       int sx = 0, sw = 0;
       uint32_t px = 0, pw = 0;
-      int aslot = 0;
+      int aslot = 0;  // index within this issuer's sub-ring
       uint32_t aph = 0;
       int ab = 0;
       int use0 = 0, use1 = 0;
-      long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const long long tstart = clock64();
-      long long tq;
+      MESW_PROF(long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
+      MESW_PROF(const long long tstart = clock64();)
+      MESW_PROF(long long tq;)
       for (int pi = 0; pi < po.np; ++pi) {
         long long pa, pb;
         po.bounds(pi, pa, pb);
         for (long long u = pa; u < pb; ++u) {
+          MESW_PROF(const long long tu = clock64();)
           const bool piece_first = (u == pa);
           const bool piece_last = (u == pb - 1);
           const int use = ab ? use1 : use0;
           if (piece_first && use > 0) {
-            tq = clock64();
+            MESW_PROF(tq = clock64();)
             mbar_wait_cluster(&S.accempty[ab], (uint32_t)((use - 1) & 1));  // both epilogues drained it
             tc_fence_after();
-            prof[5] += clock64() - tq;
+            MESW_PROF(prof[5] += clock64() - tq;)
           }
           const uint32_t d_base = tbase + (uint32_t)(ab * 2 * NP);
           const uint32_t f0 = piece_first ? 0u : 1u;
-          tq = clock64();
+          MESW_PROF(tq = clock64();)
           mbar_wait_cluster(&S.xfull[sx], px);
-          prof[0] += clock64() - tq;
+          MESW_PROF(prof[0] += clock64() - tq;)
           const uint64_t xd = xdesc0 + (uint64_t)(sx * xstride);
           if (do_base) {
-            tq = clock64();
+            MESW_PROF(tq = clock64();)
             mbar_wait_cluster(&S.wfull[sw], pw);
-            prof[1] += clock64() - tq;
-            tq = clock64();
+            MESW_PROF(prof[1] += clock64() - tq;)
+            MESW_PROF(tq = clock64();)
             tc_fence_after();
             const uint64_t wd = wdesc0 + (uint64_t)(sw * wstride);
             mma2_ss(d_base, wd, xd, id_base, f0);
@@ -643,29 +754,29 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             for (int j = 1; j < 8; ++j) mma2_ss(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
             tc2_commit(&S.wempty[sw]);
             if (++sw == p.nw) { sw = 0; pw ^= 1; }
-            prof[2] += clock64() - tq;
+            MESW_PROF(prof[2] += clock64() - tq;)
           }
           for (int q = 0; q < p.n_seg; ++q) {
-            if (seg_par < 0 || (q & 1) == seg_par) {
-              tq = clock64();
-              mbar_wait_cluster(&S.afull[aslot], aph);
-              prof[3] += clock64() - tq;
-              tq = clock64();
+            if ((q + s0) % p.n_iss == role) {
+              MESW_PROF(tq = clock64();)
+              mbar_wait_cluster(&S.afull[abase_own + aslot], aph);
+              MESW_PROF(prof[3] += clock64() - tq;)
+              MESW_PROF(tq = clock64();)
               tc_fence_after();
               const int win0 = S.segs[q].win0;
               const uint32_t id = idesc_bf16_m256(S.segs[q].winN);
               const uint32_t dd = d_base + (uint32_t)(NP + win0);
-              const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
+              const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + (abase_own + aslot) * kAColsPerSlot);
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
               const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
               mma2_ts(dd, a0, bd, id, f0);
 #pragma unroll
               for (int j = 1; j < 8; ++j) mma2_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
-              tc2_commit(&S.aempty[aslot]);
-              prof[4] += clock64() - tq;
-              prof[7]++;
+              tc2_commit(&S.aempty[abase_own + aslot]);
+              if (++aslot == na_own) { aslot = 0; aph ^= 1; }
+              MESW_PROF(prof[4] += clock64() - tq;)
+              MESW_PROF(prof[7]++;)
             }
-            if (++aslot == NA) { aslot = 0; aph ^= 1; }
           }
           tc2_commit(&S.xempty[sx]);
           if (++sx == p.nx) { sx = 0; px ^= 1; }
@@ -674,12 +785,12 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             if (ab) ++use1; else ++use0;
             if (p.n_acc == 2) ab ^= 1;
           }
+          MESW_PROF(prof[5] += clock64() - tu;)
         }
       }
       if (role == 0) MESW_STAMP(3);
-      prof[6] = clock64() - tstart;
-      if (p.tbuf)
-        for (int i = 0; i < 8; ++i) p.tbuf[4096 * 8 + (size_t)blockIdx.x * 16 + role * 8 + i] = prof[i];
+      MESW_PROF(prof[6] = clock64() - tstart;)
+      MESW_PROF(if (p.tbuf) for (int i = 0; i < 8; ++i) p.tbuf[(role < 2 ? 4096 * 8 + (size_t)blockIdx.x * 16 + role * 8 : 4096 * 48 + (size_t)blockIdx.x * 8) + i] = prof[i];)
     }
   } else if (warp < kEpiWarp0) {
     // ===================== dequant groups: own codes -> own TMEM A rows =====================
@@ -687,15 +798,14 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     const int quarter = warp & 3;
     const int mrow = quarter * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-    const int NA = p.n_aslots;
-    constexpr int WPJ = 2 * CHB / 4;
-    constexpr int MJ = 32 / WPJ;
+    constexpr int WPK = CHB / 4;  // code words per k-half of a channel
     int sc = 0;
     uint32_t pc = 0;
-    int jpar = 0, jslot = 0, juse = 0;
-    long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const long long dstart = clock64();
-    long long dq;
+    int kc0 = 0, kc1 = 0, kc2 = 0;  // jobs seen so far per issuer stream
+    const int s0 = p.w != nullptr ? 1 : 0;
+    MESW_PROF(long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
+    MESW_PROF(const long long dstart = clock64();)
+    MESW_PROF(long long dq;)
     for (int pi = 0; pi < (p.n_seg > 0 ? po.np : 0); ++pi) {
       long long pa, pb;
       po.bounds(pi, pa, pb);
@@ -703,71 +813,61 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
         for (int ch = 0; ch < p.n_chunks; ++ch) {
           const int sg0 = ch * p.segs_per_chunk;
           const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-          const int off = (grp - jpar + kDqGroups) % kDqGroups;
-          dq = clock64();
+          MESW_PROF(dq = clock64();)
           mbar_wait(&S.cfull[sc], pc);
-          dprof[0] += clock64() - dq;
+          MESW_PROF(dprof[0] += clock64() - dq;)
           const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
-          uint32_t cw[MJ][WPJ];
+          for (int q = sg0; q < sg1; ++q) {
+            const int iss = (q + s0) % p.n_iss;
+            const int k = iss == 0 ? kc0 : (iss == 1 ? kc1 : kc2);
+            if (iss == 0) ++kc0; else if (iss == 1) ++kc1; else ++kc2;
+            if ((k & 1) != grp) continue;
+            const int na = p.a_na[iss];
+            const int aslot = p.a_base[iss] + k % na;
+            const int use = k / na;
+            uint32_t cw[2 * WPK];
+            const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
 #pragma unroll
-          for (int jq = 0; jq < MJ; ++jq) {
-            const int q = sg0 + jq * kDqGroups + off;
-            if (q < sg1) {
-              const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
+            for (int kh = 0; kh < 2; ++kh)
 #pragma unroll
-              for (int kh = 0; kh < 2; ++kh)
+              for (int v = 0; v < CHB / 16; ++v) {
+                const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
+                const int w0 = kh * WPK + 4 * v;
+                cw[w0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
+              }
+            MESW_PROF(dq = clock64();)
+            if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
+            MESW_PROF(dprof[1] += clock64() - dq;)
+            MESW_PROF(dq = clock64();)
+            const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
 #pragma unroll
-                for (int v = 0; v < CHB / 16; ++v) {
-                  const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
-                  const int w0 = kh * (CHB / 4) + 4 * v;
-                  cw[jq][w0] = t4.x; cw[jq][w0 + 1] = t4.y; cw[jq][w0 + 2] = t4.z; cw[jq][w0 + 3] = t4.w;
-                }
+            for (int kh = 0; kh < 2; ++kh) {
+              uint32_t r[32];
+              dequant_chunk<DB>(&cw[kh * WPK], r);
+              tmem_st32(a0 + lane_addr + 32 * kh, r);
             }
+            MESW_PROF(dprof[2] += clock64() - dq;)
+            MESW_PROF(dq = clock64();)
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {  // 4 warps of each CTA -> leader's afull (8 arrivals)
+              if (rank == 0) mbar_arrive(&S.afull[aslot]);
+              else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
+            }
+            MESW_PROF(dprof[3] += clock64() - dq;)
+            MESW_PROF(dprof[7]++;)
           }
           mbar_arrive(&S.cempty[sc]);  // every thread: release orders its own smem reads
           if (++sc == p.nc) { sc = 0; pc ^= 1; }
-#pragma unroll
-          for (int jq = 0; jq < MJ; ++jq) {
-            const int q = sg0 + jq * kDqGroups + off;
-            if (q < sg1) {
-              const int sj = jslot + (q - sg0);
-              const int aslot = sj % NA;
-              const int use = juse + sj / NA;
-              dq = clock64();
-              if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
-              dprof[1] += clock64() - dq;
-              dq = clock64();
-              const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
-#pragma unroll
-              for (int kh = 0; kh < 2; ++kh) {
-                uint32_t r[32];
-                dequant_chunk<DB>(&cw[jq][kh * (CHB / 4)], r);
-                tmem_st32(a0 + lane_addr + 32 * kh, r);
-              }
-              dprof[2] += clock64() - dq;
-              dq = clock64();
-              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) {  // 4 warps of each CTA -> leader's afull (8 arrivals)
-                if (rank == 0) mbar_arrive(&S.afull[aslot]);
-                else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
-              }
-              dprof[3] += clock64() - dq;
-              dprof[7]++;
-            }
-          }
-          jpar = (jpar + (sg1 - sg0)) % kDqGroups;
-          jslot += sg1 - sg0;
-          while (jslot >= NA) { jslot -= NA; ++juse; }
         }
       }
     }
-    dprof[6] = clock64() - dstart;
-    if (p.tbuf && quarter == 0 && lane == 0)
-      for (int i = 0; i < 8; ++i) p.tbuf[4096 * 24 + (size_t)blockIdx.x * 16 + grp * 8 + i] = dprof[i];
+    MESW_PROF(dprof[6] = clock64() - dstart;)
+    MESW_PROF(if (p.tbuf && quarter == 0 && lane == 0) for (int i = 0; i < 8; ++i) p.tbuf[4096 * 24 + (size_t)blockIdx.x * 16 + grp * 8 + i] = dprof[i];)
   } else {
     // ===================== epilogue warpgroup (own column group) =====================
+    pdl_wait();  // reads x / residual, writes y / workspace: previous kernel must be complete
     const int quarter = warp & 3;
     const int mrow = quarter * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
@@ -839,91 +939,33 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       acc_use[ab]++;
       if (p.n_acc == 2) ab ^= 1;
       if (!whole) {
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (gtid == 0 && pi == po.np - 1) MESW_STAMP(1);
+        named_bar_sync(1, 128);  // the partial stores above happen-before gtid 0's release
         // contributors to this column group: the pairs owning its first/last unit
         const long long first_u = (long long)cgp * p.n_ks, last_u = first_u + p.n_ks - 1;
         const int p_first = unit_owner(first_u, T2, (int)G2), p_last = unit_owner(last_u, T2, (int)G2);
         if (gtid == 0) {
-          const int prev = atomicAdd(&p.counters[cg], 1);
+          // acq_rel: releases this CTA's partials (ordered by the barrier) and, for the last
+          // arriver, acquires every other contributor's (their release increments)
+          const int prev = atom_add_acq_rel_gpu(&p.counters[cg], 1);
           S.flag = (prev == p_last - p_first) ? 1 : 0;
         }
         named_bar_sync(1, 128);
-        if (gtid == 0 && pi == po.np - 1) MESW_STAMP(2);
         if (S.flag) {
-          long long ep[4] = {0, 0, 0, 0}, ec = clock64();
-          __threadfence();
-          ep[3] = clock64() - ec;
-          const size_t slot_floats = (size_t)2 * NP * kUnitN;
-          for (int t0 = 0; t0 < NP; t0 += 16) {
-            ec = clock64();
-            const int sg = S.tok2seg[t0];
-            int cb0 = t0 / 2, cb1 = HP + t0 / 2, cd0 = -1, cd1 = -1;
-            if (sg >= 0) {
-              const SegDesc& sd = S.segs[sg];
-              const int dw = (t0 - sd.win0) / 2;
-              cd0 = NP + sd.win0 + dw;
-              cd1 = NP + sd.win0 + sd.winN / 2 + dw;
+          if (pi == po.np - 1) {
+            // final piece: handed to all 16 warps of the CTA after the role loops (their
+            // chunks reduce in parallel: the tail of the launch is one L2 round trip deep)
+            if (gtid == 0) {
+              S.fin.cg = cg; S.fin.cgp = cgp; S.fin.p_first = p_first; S.fin.p_last = p_last;
+              S.fin.fast = fast ? 1 : 0; S.fin.on = 1;
             }
-            float vb[16], vd[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) vb[i] = vd[i] = 0.f;
-            // all contributors' loads of this 16-row chunk are issued before any is used (one
-            // L2 round trip per chunk, not one per contributor); summed in fixed pair order
-            for (int pb = p_first; pb <= p_last; pb += kRedBatch) {
-              float lb[kRedBatch][16], ld[kRedBatch][16];
-#pragma unroll
-              for (int b = 0; b < kRedBatch; ++b) {
-                const int pp = pb + b;
-                if (pp <= p_last) {
-                  const long long pu0 = (long long)pp * T2 / G2;
-                  const int s2 = 2 * (2 * pp + (int)rank) + ((int)(pu0 / p.n_ks) == cgp ? 0 : 1);
-                  const float* src = p.ws + (size_t)s2 * slot_floats + mrow;
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) {
-                    lb[b][i] = __ldcg(src + (size_t)(cb0 + i) * kUnitN);
-                    lb[b][8 + i] = __ldcg(src + (size_t)(cb1 + i) * kUnitN);
-                  }
-                  if (cd0 >= 0) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                      ld[b][i] = __ldcg(src + (size_t)(cd0 + i) * kUnitN);
-                      ld[b][8 + i] = __ldcg(src + (size_t)(cd1 + i) * kUnitN);
-                    }
-                  }
-                }
-              }
-#pragma unroll
-              for (int b = 0; b < kRedBatch; ++b) {
-                if (pb + b <= p_last) {
-#pragma unroll
-                  for (int i = 0; i < 16; ++i) vb[i] += lb[b][i];
-                  if (cd0 >= 0) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) vd[i] += ld[b][i];
-                  }
-                }
-              }
+          } else {
+            for (int t0 = 0; t0 < NP; t0 += 16) {
+              EpiPre pre;
+              epi_prefetch(p, S, cg, mrow, t0, fast, pre);
+              reduce_chunk(p, S, cg, cgp, (int)rank, mrow, t0, p_first, p_last, fast, pre, nullptr);
             }
-            if (!has_w) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) vb[i] = 0.f;
-            }
-            float vsum = 0.f;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) vsum += vb[i] + vd[i];
-            if (vsum == 12345.f) S.flag = 2;  // forces the partial loads to complete here (timing)
-            ep[0] += clock64() - ec; ec = clock64();
-            epi_store16(p, S, cg, mrow, t0, vb, vd, fast, pre);
-            ep[1] += clock64() - ec; ec = clock64();
-            if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
-            ep[2] += clock64() - ec;
+            if (gtid == 0) p.counters[cg] = 0;  // self-reset for the next launch
           }
-          if (gtid == 0 && pi == po.np - 1) MESW_STAMP(4);
-          if (gtid == 0 && pi == po.np - 1 && p.tbuf)
-            for (int i = 0; i < 4; ++i) p.tbuf[4096 * 40 + (size_t)blockIdx.x * 16 + i] = ep[i];
-          if (gtid == 0) p.counters[cg] = 0;  // self-reset for the next launch
         }
       }
       named_bar_sync(1, 128);  // xsal / flag reuse by the next piece
@@ -931,8 +973,45 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     }
   }
 
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) MESW_STAMP(1);
+  if (S.fin.on) {  // this CTA is the last contributor of its final column group (acquired above)
+    if (threadIdx.x == 0) MESW_STAMP(2);
+    const int fcg = S.fin.cg, fcgp = S.fin.cgp, pf = S.fin.p_first, pl = S.fin.p_last;
+    const bool ffast = S.fin.fast != 0;
+    const int fm = threadIdx.x % kUnitN;
+    // every contributor's whole slot in one bulk copy each, into the (now idle) smem ring
+    const size_t slot_bytes = (size_t)2 * NP * kUnitN * sizeof(float);
+    const bool staged = (size_t)(pl - pf + 1) * slot_bytes <= (size_t)p.ring_bytes;
+    if (staged && threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy partials -> TMA reads
+      mbar_arrive_expect_tx(&S.finbar, (uint32_t)((pl - pf + 1) * slot_bytes));
+      const long long T2 = p.T, G2 = p.G / 2;
+      for (int pp = pf; pp <= pl; ++pp) {
+        const long long pu0 = (long long)pp * T2 / G2;
+        const int s2 = 2 * (2 * pp + (int)rank) + ((int)(pu0 / p.n_ks) == fcgp ? 0 : 1);
+        bulk_g2s(ring + (size_t)(pp - pf) * slot_bytes, p.ws + (size_t)s2 * (slot_bytes / sizeof(float)),
+                 (uint32_t)slot_bytes, &S.finbar);
+      }
+    }
+    MESW_PROF(long long fp[4] = {0, 0, 0, 0}; long long fq = clock64();)
+    for (int t0 = 16 * (threadIdx.x / kUnitN); t0 < NP; t0 += 16 * (kThreads / kUnitN)) {
+      EpiPre pre;
+      epi_prefetch(p, S, fcg, fm, t0, ffast, pre);  // in flight with the bulk copies
+      MESW_PROF(fp[0] += clock64() - fq; fq = clock64();)
+      if (staged) mbar_wait(&S.finbar, 0);
+      MESW_PROF(fp[1] += clock64() - fq; fq = clock64();)
+      reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre,
+                   staged ? reinterpret_cast<const float*>(ring) : nullptr);
+      MESW_PROF(fp[2] += clock64() - fq; fq = clock64();)
+    }
+    MESW_PROF(fp[3] = staged ? (pl - pf + 1) : -1;)
+    MESW_PROF(if (p.tbuf && threadIdx.x == 0) for (int i = 0; i < 4; ++i) p.tbuf[4096 * 40 + (size_t)blockIdx.x * 16 + i] = fp[i];)
+    if (threadIdx.x == 0) p.counters[S.fin.cg] = 0;
+    if (threadIdx.x == 0) MESW_STAMP(4);
+  }
   cluster_sync_all();  // the peer's MMAs / TMEM reads are complete before deallocation
   if (warp == kMmaWarp) {
     tc_fence_after();
@@ -954,13 +1033,15 @@ int launch(const LinearParams& p, size_t smem, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;  // CTA pairs for cta_group::2
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = mesw_pdl_enabled() ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, me_linear_tc_kernel<DB>, p);
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("me_linear");
@@ -1053,41 +1134,82 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   p.cbytes = p.segs_per_chunk * CB;
   const size_t budget = 232448 - ring_offset();
   // ring depths: prefer (x 3, codes 3, weights >= 3); shrink x/codes first when rows are many
-  p.nx = getenv("MESW_NX") ? atoi(getenv("MESW_NX")) : 3;
-  p.nc = p.n_chunks > 0 ? 3 : 0;
+  // Ring depths: one producer thread walks the rings in unit order, so every ring gets the
+  // same lookahead D (units); D is the largest that fits (<= kMaxStages, >= 2).
   for (;;) {
-    const size_t used = (size_t)p.nx * p.xbytes + (size_t)p.nc * p.cbytes + 1024;
-    p.nw = a->w ? (int)((budget > used ? budget - used : 0) / kUnitWBytes) : 0;
-    if (p.nw > kMaxStages) p.nw = kMaxStages;
-    if (!a->w || p.nw >= 3) break;
-    if (p.nx > 2) { --p.nx; continue; }
-    if (p.nc > 2) { --p.nc; continue; }
-    if (p.nw >= 2) break;
+    const size_t per_unit = (a->w ? (size_t)kUnitWBytes : 0) + (size_t)p.xbytes + (size_t)p.n_chunks * p.cbytes;
+    int D = (int)((budget - 1024) / per_unit);
+    if (D > kMaxStages) D = kMaxStages;
+    if (D >= 2) {
+      p.nx = D;
+      p.nw = a->w ? D : 0;
+      p.nc = std::min(kMaxCStages, D * p.n_chunks);
+      break;
+    }
+    // code-heavy launches: two units of weights / activations, the code ring gets the rest
+    const size_t wx = 2 * ((a->w ? (size_t)kUnitWBytes : 0) + (size_t)p.xbytes) + 1024;
+    const int nc = budget > wx ? (int)std::min<size_t>(kMaxCStages, (budget - wx) / p.cbytes) : 0;
+    if (nc >= 2) {
+      p.nx = 2;
+      p.nw = a->w ? 2 : 0;
+      p.nc = nc;
+      break;
+    }
     if (p.segs_per_chunk > kDqGroups) {  // smaller code chunks
       p.segs_per_chunk = (p.segs_per_chunk / 2 + kDqGroups - 1) / kDqGroups * kDqGroups;
       p.n_chunks = (p.n_seg + p.segs_per_chunk - 1) / p.segs_per_chunk;
       p.cbytes = p.segs_per_chunk * CB;
       continue;
     }
-    return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory: fewer than 2 weight stages");
+    return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory: fewer than 2 pipeline stages");
   }
   p.xo = 0;
   p.co = p.nx * p.xbytes;
   p.wo = (p.co + p.nc * p.cbytes + 1023) & ~1023;
-  const size_t smem = ring_offset() + (size_t)p.wo + (size_t)p.nw * kUnitWBytes;
+  size_t smem = ring_offset() + (size_t)p.wo + (size_t)p.nw * kUnitWBytes;
   if (smem > 232448) return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory overflow");
-  // TMEM: n_acc buffers of [D_base NP | D_delta NP] columns, then the A ring (64-col slots)
-  p.n_acc = (4 * p.NP + 2 * kAColsPerSlot <= kTmemCols) ? 2 : 1;
-  int na = (kTmemCols - p.n_acc * 2 * p.NP) / kAColsPerSlot;
-  if (na > kMaxASlots) na = kMaxASlots;
-  na -= na % kDqGroups;
-  if (na < kDqGroups) return mesw_fail(MESW_ERR_UNSUPPORTED, "tensor memory: too many rows for the A ring");
-  p.n_aslots = na;
-  p.a_col0 = kTmemCols - na * kAColsPerSlot;
+  smem = 232448;  // one CTA per SM regardless: the slack stages the final stream-K reduction
+  p.ring_bytes = (int)(smem - ring_offset());
+  // TMEM: n_acc buffers of [D_base NP | D_delta NP] columns, then the A ring (64-col job slots)
+  // MMA issuers: streams (base tile, then one per segment) dealt round-robin.  Each issuer
+  // with delta jobs needs its own even A sub-ring (>= 2 slots of 64 TMEM columns); prefer
+  // two accumulator buffers, then more issuers.
   {
-    int iss = (p.w ? 1 : 0) + p.n_seg;
-    if (getenv("MESW_ISS")) iss = std::min(iss, atoi(getenv("MESW_ISS")));
-    p.n_iss = iss < kMaxIssuers ? (iss < 1 ? 1 : iss) : kMaxIssuers;
+    int want = (p.w ? 1 : 0) + p.n_seg;
+    if (getenv("MESW_ISS")) want = std::min(want, atoi(getenv("MESW_ISS")));
+    want = std::max(1, std::min(want, kMaxIssuers));
+    bool done = false;
+    for (int n_acc = 2; n_acc >= 1 && !done; --n_acc) {
+      for (int iss = want; iss >= 1 && !done; --iss) {
+        int n_delta = 0;  // issuers that own at least one segment
+        for (int i = 0; i < iss; ++i) {
+          bool any = false;
+          for (int q = 0; q < p.n_seg; ++q) any |= ((q + (p.w ? 1 : 0)) % iss == i);
+          n_delta += any ? 1 : 0;
+        }
+        const int cols = kTmemCols - n_acc * 2 * p.NP;
+        int slots = cols / kAColsPerSlot;
+        if (slots > kMaxASlots) slots = kMaxASlots;
+        if (cols < 0 || (n_delta > 0 && slots < 2 * n_delta)) continue;
+        const int per = n_delta > 0 ? (slots / n_delta) & ~1 : 0;
+        int base = 0;
+        for (int i = 0; i < 3; ++i) { p.a_base[i] = 0; p.a_na[i] = 0; }
+        for (int i = 0; i < iss; ++i) {
+          bool any = false;
+          for (int q = 0; q < p.n_seg; ++q) any |= ((q + (p.w ? 1 : 0)) % iss == i);
+          if (!any) continue;
+          p.a_base[i] = base;
+          p.a_na[i] = per;
+          base += per;
+        }
+        p.n_acc = n_acc;
+        p.n_iss = iss;
+        p.n_aslots = base;
+        p.a_col0 = kTmemCols - base * kAColsPerSlot;
+        done = true;
+      }
+    }
+    if (!done) return mesw_fail(MESW_ERR_UNSUPPORTED, "tensor memory: too many rows for the A ring");
   }
 
   cudaStream_t s = (cudaStream_t)stream;

@@ -25,9 +25,10 @@ buf = np.zeros(56 * 4096, np.uint64)
 _lib.check(L.mesw_debug_timing_copy(buf.ctypes.data, G))
 t = buf[:G * 8].reshape(G, 8).astype(np.int64)
 prof = buf[4096 * 8:4096 * 8 + G * 16].reshape(G, 2, 8).astype(np.int64)
+prof3 = buf[4096 * 48:4096 * 48 + G * 8].reshape(G, 8).astype(np.int64)
 dprof = buf[4096 * 24:4096 * 24 + G * 16].reshape(G, 2, 8).astype(np.int64)
 t0 = t[:, 0].min()
-names = ["start", "ws_fenced", "flag_known", "mma_done", "red_done", "last_accfull", "last_tmem", "last_end"]
+names = ["start", "all_synced", "fin_fenced", "mma_done", "red_done", "last_accfull", "last_tmem", "last_end"]
 print(f"m={m} n={n} E={E} rows={rows}  (us from first CTA start)")
 for i, nm in enumerate(names):
     v = (t[:, i] - t0) / 1e3
@@ -35,14 +36,15 @@ for i, nm in enumerate(names):
     if v.size:
         print(f"  {nm:12s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f}")
 
-pm = ["wait_x", "wait_w", "base_issue", "wait_afull", "delta_issue", "wait_accempty", "total", "jobs"]
+pm = ["wait_x", "wait_w", "base_issue", "wait_afull", "delta_issue", "unit_sum", "total", "jobs"]
 pd = ["wait_cfull", "wait_aempty", "dequant+st", "wait_st+arrive", "-", "-", "total", "jobs"]
 lead = prof[0::2, 0, :]
 print("  mma   ", " ".join(f"{pm[i]}={np.median(lead[:, i]):.0f}" for i in range(8)))
 print("  mma2  ", " ".join(f"{pm[i]}={np.median(prof[0::2, 1, i]):.0f}" for i in range(8)))
+print("  mma3  ", " ".join(f"{pm[i]}={np.median(prof3[0::2, i]):.0f}" for i in range(8)))
 for g in range(2):
     for r, nm in ((0, "lead"), (1, "peer")):
         print(f"  deq{g} {nm}", " ".join(f"{pd[i]}={np.median(dprof[r::2, g, i]):.0f}" for i in range(8) if pd[i] != "-"))
 eprof = buf[4096 * 40:4096 * 40 + G * 16].reshape(G, 16).astype(np.int64)
 sel = eprof[:, 0] > 0
-print("  red (last arrivers, cycles):", " ".join(f"{n}={np.median(eprof[sel, i]):.0f}" for i, n in enumerate(["loads", "store", "prefetch", "fence"])), f"n={sel.sum()}")
+print("  final red (cycles):", " ".join(f"{n}={np.median(eprof[sel, i]):.0f}/{np.max(eprof[sel, i]):.0f}" for i, n in enumerate(["prefetch_issue", "stage_wait", "reduce+store", "ncontrib"])), f"n={sel.sum()}")
