@@ -227,6 +227,19 @@ int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int ld, int32_t
 int mesw_advance_positions(int32_t* d_pos, int32_t* d_len, int B, int ctx_max, int wrap_to,
                            void* stream);
 
+/* ------------------------------------------------ K4: model-level router
+ * Replaces SPEC router.classify for a batch of B queries:
+ * multinomial Naive Bayes over FNV-1a-hashed character 2/3-grams (2^16 buckets),
+ * hashing and f64 summation order as pinned in oracle/router.py.
+ *   d_codepoints  int32 Unicode code points of all queries, concatenated
+ *   d_offsets     int64[B+1]: query q = code points [off[q], off[q+1])
+ *   d_loglik      f32[D][65536], d_logprior f32[D], 1 <= D <= 6
+ * Outputs: d_domain[B] (argmax, ties -> lowest id), d_conf[B] (softmax of the
+ * winner), d_prior_only[B] (1 when the query has no n-gram; may be NULL).      */
+int mesw_router_classify(const int32_t* d_codepoints, const int64_t* d_offsets, int B,
+                         const float* d_loglik, const float* d_logprior, int D, int32_t* d_domain,
+                         float* d_conf, int32_t* d_prior_only, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,86 @@
+"""Router oracle (SPEC.md:516-573 restatement) and the host side of the drop-in router."""
+import numpy as np
+import pytest
+
+from oracle import router as orc
+from paper_2406_09041_b200 import router as pr
+from paper_2406_09041_b200.errors import BadMagicError, TruncatedArtifactError
+from router_data import DOMAINS, make_records
+
+
+def test_fnv1a_known_answers():
+    # published FNV-1a 32-bit test vectors
+    assert orc.fnv1a32(b"") == 0x811C9DC5
+    assert orc.fnv1a32(b"a") == 0xE40C292C
+    assert orc.fnv1a32(b"foobar") == 0xBF9CF968
+
+
+def test_ngram_order_and_package_agree():
+    q = "ab漢c"
+    b = orc.ngram_buckets(q)
+    assert len(b) == 3 + 2  # 2-grams then 3-grams
+    assert b[0] == orc.fnv1a32("ab".encode()) & 0xFFFF
+    assert b[3] == orc.fnv1a32("ab漢".encode()) & 0xFFFF
+    for s in ["", "x", "hello world", "翻译这个句子", q * 7]:
+        assert list(pr.ngram_buckets(s)) == orc.ngram_buckets(s)
+
+
+def test_train_matches_oracle_bitwise():
+    recs = make_records(20, seed=1)
+    a = orc.train_router(recs, DOMAINS)
+    b = pr.train_router(recs, DOMAINS)
+    assert a.domains == b.domains
+    assert np.array_equal(a.logprior.view(np.uint32), b.logprior.view(np.uint32))
+    assert np.array_equal(a.loglik.view(np.uint32), b.loglik.view(np.uint32))
+
+
+def test_spec_examples_oracle():
+    recs = make_records(100, seed=2)
+    r = orc.train_router(recs, DOMAINS)
+    held = make_records(25, seed=3)
+    acc = np.mean([r.domains[orc.classify(r, q)[0]] == d for q, d in held])
+    assert acc == 1.0  # SPEC.md:544 separable keyword domains
+    # single-domain router always predicts it
+    one = orc.train_router([(q, "code") for q, d in recs if d == "code"], ("code",))
+    assert all(orc.classify(one, q)[0] == 0 for q, _ in held[:20])
+    # empty query, uniform priors -> lowest id, flagged prior-only
+    d, conf, flag = orc.classify(r, "")
+    assert d == 0 and flag and abs(conf - 0.25) < 1e-6
+    # repeating the query does not change the argmax
+    for q, _ in held[:20]:
+        assert orc.classify(r, q)[0] == orc.classify(r, q + q)[0]
+
+
+def test_train_errors():
+    with pytest.raises(ValueError):
+        orc.train_router([("x y", "code")], ("code", "math"))
+    with pytest.raises(ValueError):
+        pr.train_router([("x y", "code")], ("code", "math"))
+    with pytest.raises(ValueError):
+        pr.train_router([("x", "nope")], ("code",))
+    with pytest.raises(ValueError):
+        pr.Router(tuple("abcdefg"), np.zeros(7, np.float32), np.zeros((7, pr.N_BUCKETS), np.float32))
+
+
+def test_mert_roundtrip_and_errors():
+    r = pr.train_router(make_records(5, seed=4), DOMAINS)
+    blob = pr.save_router(r)
+    r2 = pr.load_router(blob)
+    assert r2.domains == r.domains
+    assert np.array_equal(r2.loglik, r.loglik) and np.array_equal(r2.logprior, r.logprior)
+    with pytest.raises(BadMagicError):
+        pr.load_router(b"XXXX" + blob[4:])
+    with pytest.raises(TruncatedArtifactError):
+        pr.load_router(blob[:-1])
+
+
+def test_render_prompt():
+    doms = [("Instruct", "For general guidance, explanations, or broad advice."),
+            ("Code", "For programming-related queries, like debugging or coding."),
+            ("Math", "For mathematical inquiries, such as problems or theories."),
+            ("Chinese Language Expert", "For inquiries related to the Chinese language.")]
+    s = pr.render_prompt("sort a list", doms)
+    assert "Query: sort a list" in s and "B) Code" in s
+    assert "Classify the query based on the required expertise." in s
+    with pytest.raises(ValueError):
+        pr.render_prompt("q", doms + doms)
