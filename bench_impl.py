@@ -106,6 +106,17 @@ def reference_arm(args):
 
 # ------------------------------------------------------------------ GPU timing
 
+def _traffic(key):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json), or None."""
+    import json
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            return json.load(f)[key]["traffic"]
+    except Exception:
+        return None
+
+
 def _device_c1(torch, W, arts, replicas: int):
     from paper_2406_09041_b200.device import DeviceDelta, DeviceWeight, ExpertTable
     sets = []
@@ -193,7 +204,7 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
                    "l2": "3 rotating weight/delta replicas (489 MB) > 126 MB L2",
                    "parallelism": f"expert-sharded replicas x{ws}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": _traffic("c1"), "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_launch, "kernel": "me_linear_tc_kernel<2> (cta_group::2 pairs)"},
         "e2e": {"value": ws * C1_B / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(xh.numel() * 2),
                 "d2h_bytes_per_step": int(yh.numel() * 2)},

@@ -30,21 +30,26 @@ def _expert_names(E):
     return [base[e] if e < 3 else f"expert{e}" for e in range(E)]
 
 
-def build_engine(B, E, seed=0, n_layers=None, device="cuda"):
+def build_engine(B, E, seed=0, n_layers=None, device="cuda", experts=None, requests=None):
+    """Engine with the base (replicated) and experts `experts` (global ids; default
+    0..E-1) resident; batch = `requests` (global expert id per request; default
+    round-robin over the resident experts)."""
     from paper_2406_09041_b200 import compress, synth
     from paper_2406_09041_b200.mistral import MistralMultiExpert
+    experts = list(range(E)) if experts is None else list(experts)
     shape = synth.MistralShape()
-    eng = MistralMultiExpert(shape, max_batch=min(192, B + 16 * E), ctx_max=CTX, device=device,
+    eng = MistralMultiExpert(shape, max_batch=min(192, B + 16 * len(experts)), ctx_max=CTX, device=device,
                              n_layers=n_layers)
     eng.load_synthetic_base(seed=seed)
     shapes = synth.mistral_expert_shapes(shape, eng.n_layers)
-    names = _expert_names(E)
-    for e in range(E):
-        blob = synth.synthetic_expert_artifact(1000 * (seed + 1) + e, shapes, names[e])
+    names = _expert_names(max(experts) + 1)
+    for e in experts:
+        blob = synth.synthetic_expert_artifact(1000 + e, shapes, names[e])
         eng.add_expert(names[e], compress.deserialize_artifact(blob))
         del blob
-    experts = [names[t % E] for t in range(B)]
-    eng.set_batch(experts, [PROMPT] * B)
+    if requests is None:
+        requests = [experts[t % len(experts)] for t in range(B)]
+    eng.set_batch([names[e] for e in requests], [PROMPT] * len(requests))
     eng.fill_random_kv(PROMPT, seed=seed + 7)
     return eng
 
@@ -53,7 +58,14 @@ def run_c2(args, ws, rank, local, ClockSampler, peaks):
     import torch
     B = args.batch or DEFAULT_B
     E = args.experts
-    eng = build_engine(B, E, seed=rank)
+    # expert-sharded weak scaling: E experts per GPU (E*ws in total, expert e on rank e mod ws),
+    # base replicated (seed 0 everywhere); rank 0 assigns B*ws requests round-robin over all
+    # experts and dispatches each to its owner -- a host control message, no data collective
+    from paper_2406_09041_b200.shard import Placement, dispatch
+    pl = Placement(E * ws, ws)
+    reqs = [(i, i % (E * ws), None) for i in range(B * ws)] if rank == 0 else None
+    mine = dispatch(reqs, pl, rank) if ws > 1 else reqs
+    eng = build_engine(B, E, seed=0, experts=pl.local_experts(rank), requests=[r[1] for r in mine])
     g = torch.Generator(device="cuda")
     g.manual_seed(5)
     R = eng.B  # engine rows (expert groups padded to 16-row boundaries)
@@ -131,7 +143,7 @@ def run_c2(args, ws, rank, local, ClockSampler, peaks):
         import json
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
             tr = json.load(f).get(f"c2_B{B}_E{E}")
-            traffic = tr
+            traffic = tr["traffic"] if tr else None  # dram bytes of one step's linear launches
     except Exception:
         pass
 
