@@ -32,10 +32,10 @@
 
 namespace mesw {
 
-constexpr int kDqGroups = 2;  // dequant warpgroups: group (k % 2) expands issuer stream job k
-// warp roles: 0 producer (codes, weight tiles, activations), 1-3 MMA issuers, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
-constexpr int kProdWarp = 0, kMmaWarp = 1;
-constexpr int kMaxIssuers = 3;  // warps 1..3
+constexpr int kDqGroups = 2;  // dequant warpgroups: group g expands k-half g of every job
+// warp roles: 0 weight-tile producer, 1-2 MMA issuers, 3 code + activation producer, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
+constexpr int kProdWarp = 0, kMmaWarp = 1, kXCProdWarp = 3;
+constexpr int kMaxIssuers = 2;  // warps 1..2
 constexpr int kDqWarp0 = 4, kEpiWarp0 = kDqWarp0 + 4 * kDqGroups;
 constexpr int kThreads = (kEpiWarp0 + 4) * 32;  // 16 warps
 constexpr int kTmemCols = 512;
@@ -90,10 +90,10 @@ struct LinearParams {
   int nc, co, cbytes, segs_per_chunk, n_chunks;
   // tensor memory: n_acc accumulator buffers of 2*NP columns, A ring from a_col0
   int n_acc, n_aslots, a_col0;
-  // A ring split per MMA issuer: issuer i owns slots [a_base[i], a_base[i] + a_na[i]) (a_na even)
-  // and consumes its jobs in order; dequant group (k % 2) writes issuer i's k-th job.  Every
-  // slot is therefore written by one group and read by one issuer, in sequence, so the
-  // mbarrier parity waits on it can never alias a phase two steps away.
+  // A ring split per MMA issuer: issuer i owns slots [a_base[i], a_base[i] + a_na[i]) and
+  // consumes its jobs in order; both dequant groups walk every job in the same order.  Every
+  // slot is therefore filled and drained in one sequence, so the mbarrier parity waits on
+  // it can never alias a phase two steps away.
   int a_base[3], a_na[3];
   int ring_bytes;  // dynamic shared memory past the Smem header
   int n_iss;  // MMA issuer threads (a tcgen05.mma stream runs ~60-85 cycles/instr per issuer)
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     for (int i = 0; i < p.nx; ++i) { mbar_init(&S.xfull[i], peer_relay); mbar_init(&S.xempty[i], p.n_iss); }
     for (int i = 0; i < p.nw; ++i) { mbar_init(&S.wfull[i], peer_relay); mbar_init(&S.wempty[i], 1); }
     for (int i = 0; i < p.nc; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 128 * kDqGroups); }
-    for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 8); mbar_init(&S.aempty[i], 1); }
+    for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 16); mbar_init(&S.aempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], p.n_iss); mbar_init(&S.accempty[i], 8); }
     mbar_init(&S.finbar, 1);
     fence_mbar_init();
@@ -619,63 +619,80 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   if (threadIdx.x == 0) MESW_STAMP(0);
   pdl_trigger();
 
-  if (warp == kProdWarp) {
-    // ===================== producer (own column group / own x half), one thread =====================
-    // per unit: code chunks (the dequant groups run ahead), weight tile, activation half-tile
+  if (warp == kProdWarp || warp == kXCProdWarp) {
+    // ===================== producers (own column group / own x half) =====================
+    // warp 0: weight tiles (static: streamed from the first cycle, even before the previous
+    // kernel completes -- PDL); warp 3: per unit the code chunks (static, prefetched before
+    // the PDL wait) and the activation half-tile (after it).  One thread each.
     if (lane == 0) {
       uint64_t evict_first;  // weights / codes are streamed once: do not let them evict partials
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
-      int sw = 0, sx = 0, sc = 0;
-      uint32_t pw = 0, px = 0, pc = 0;
-      bool wfirst = true, xfirst = true, cfirst = true;
-      // Codes and weight tiles are static: the first ring's worth is requested before
-      // waiting for the previous kernel (PDL), activations only after it completed.
-      int n_pre = 0;
-      auto issue_static = [&](int cg, int ks) {
-        const long long unit = (long long)cg * p.n_ks + ks;  // this CTA's unit
-        for (int ch = 0; ch < p.n_chunks; ++ch) {
-          const int sg0 = ch * p.segs_per_chunk;
-          const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-          if (!cfirst) mbar_wait(&S.cempty[sc], pc ^ 1);
-          mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
-          for (int q = sg0; q < sg1; ++q)
-            bulk_g2s_hint(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB,
-                          S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[sc], evict_first);
-          if (++sc == p.nc) { sc = 0; pc ^= 1; cfirst = false; }
-        }
-        if (has_w) {
-          if (!wfirst) mbar_wait(&S.wempty[sw], pw ^ 1);
-          mbar_arrive_expect_tx(&S.wfull[sw], kUnitWBytes);
-          bulk_g2s_hint(ring + p.wo + (size_t)sw * kUnitWBytes, p.w + (size_t)unit * kUnitWBytes, kUnitWBytes,
-                        &S.wfull[sw], evict_first);
-          if (++sw == p.nw) { sw = 0; pw ^= 1; wfirst = false; }
-        }
-      };
-      {
-        const int D = min(p.nx, p.nc > 0 ? p.nc / max(p.n_chunks, 1) : p.nx);
-        for (int pi = 0; pi < po.np && n_pre < D; ++pi) {
+      if (warp == kProdWarp) {
+        int sw = 0;
+        uint32_t pw = 0;
+        bool wfirst = true;
+        for (int pi = 0; pi < (has_w ? po.np : 0); ++pi) {
           long long pa, pb;
           po.bounds(pi, pa, pb);
           const int cgp = po.cg_of(pi);
-          for (long long u = pa; u < pb && n_pre < D; ++u, ++n_pre)
-            issue_static(2 * cgp + (int)rank, (int)(u - (long long)cgp * p.n_ks));
+          const int cg = 2 * cgp + (int)rank;
+          for (long long u = pa; u < pb; ++u) {
+            const long long unit = (long long)cg * p.n_ks + (u - (long long)cgp * p.n_ks);
+            if (!wfirst) mbar_wait(&S.wempty[sw], pw ^ 1);
+            mbar_arrive_expect_tx(&S.wfull[sw], kUnitWBytes);
+            bulk_g2s_hint(ring + p.wo + (size_t)sw * kUnitWBytes, p.w + (size_t)unit * kUnitWBytes, kUnitWBytes,
+                          &S.wfull[sw], evict_first);
+            if (++sw == p.nw) { sw = 0; pw ^= 1; wfirst = false; }
+          }
         }
-      }
-      pdl_wait();
-      int idx = 0;
-      for (int pi = 0; pi < po.np; ++pi) {
-        long long pa, pb;
-        po.bounds(pi, pa, pb);
-        const int cgp = po.cg_of(pi);
-        const int cg = 2 * cgp + (int)rank;
-        for (long long u = pa; u < pb; ++u, ++idx) {
-          const int ks = (int)(u - (long long)cgp * p.n_ks);
-          if (idx >= n_pre) issue_static(cg, ks);
-          if (!xfirst) mbar_wait(&S.xempty[sx], px ^ 1);
-          mbar_arrive_expect_tx(&S.xfull[sx], (uint32_t)p.xbytes);
-          bulk_g2s(ring + p.xo + (size_t)sx * p.xbytes, p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK,
-                   p.xbytes, &S.xfull[sx]);
-          if (++sx == p.nx) { sx = 0; px ^= 1; xfirst = false; }
+      } else {
+        int sx = 0, sc = 0;
+        uint32_t px = 0, pc = 0;
+        bool xfirst = true, cfirst = true;
+        auto issue_codes = [&](int cg, int ks) {
+          const long long unit = (long long)cg * p.n_ks + ks;  // this CTA's unit
+          for (int ch = 0; ch < p.n_chunks; ++ch) {
+            const int sg0 = ch * p.segs_per_chunk;
+            const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
+            if (!cfirst) mbar_wait(&S.cempty[sc], pc ^ 1);
+            if (p.dbg & 32) {
+              mbar_arrive(&S.cfull[sc]);
+            } else {
+              mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
+              for (int q = sg0; q < sg1; ++q)
+                bulk_g2s_hint(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB,
+                              S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[sc], evict_first);
+            }
+            if (++sc == p.nc) { sc = 0; pc ^= 1; cfirst = false; }
+          }
+        };
+        int n_pre = 0;  // units whose codes go out before the PDL wait
+        if (p.n_chunks > 0) {
+          const int D = p.nc / p.n_chunks;
+          for (int pi = 0; pi < po.np && n_pre < D; ++pi) {
+            long long pa, pb;
+            po.bounds(pi, pa, pb);
+            const int cgp = po.cg_of(pi);
+            for (long long u = pa; u < pb && n_pre < D; ++u, ++n_pre)
+              issue_codes(2 * cgp + (int)rank, (int)(u - (long long)cgp * p.n_ks));
+          }
+        }
+        pdl_wait();
+        int idx = 0;
+        for (int pi = 0; pi < po.np; ++pi) {
+          long long pa, pb;
+          po.bounds(pi, pa, pb);
+          const int cgp = po.cg_of(pi);
+          const int cg = 2 * cgp + (int)rank;
+          for (long long u = pa; u < pb; ++u, ++idx) {
+            const int ks = (int)(u - (long long)cgp * p.n_ks);
+            if (idx >= n_pre && p.n_chunks > 0) issue_codes(cg, ks);
+            if (!xfirst) mbar_wait(&S.xempty[sx], px ^ 1);
+            mbar_arrive_expect_tx(&S.xfull[sx], (uint32_t)p.xbytes);
+            bulk_g2s(ring + p.xo + (size_t)sx * p.xbytes,
+                     p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK, p.xbytes, &S.xfull[sx]);
+            if (++sx == p.nx) { sx = 0; px ^= 1; xfirst = false; }
+          }
         }
       }
     }
@@ -749,15 +766,17 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             MESW_PROF(tq = clock64();)
             tc_fence_after();
             const uint64_t wd = wdesc0 + (uint64_t)(sw * wstride);
-            mma2_ss(d_base, wd, xd, id_base, f0);
+            if (!(p.dbg & 8)) {
+              mma2_ss(d_base, wd, xd, id_base, f0);
 #pragma unroll
-            for (int j = 1; j < 8; ++j) mma2_ss(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
+              for (int j = 1; j < 8; ++j) mma2_ss(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
+            }
             tc2_commit(&S.wempty[sw]);
             if (++sw == p.nw) { sw = 0; pw ^= 1; }
             MESW_PROF(prof[2] += clock64() - tq;)
           }
           for (int q = 0; q < p.n_seg; ++q) {
-            if ((q + s0) % p.n_iss == role) {
+            if (!(p.dbg & 16) && (q + s0) % p.n_iss == role) {
               MESW_PROF(tq = clock64();)
               mbar_wait_cluster(&S.afull[abase_own + aslot], aph);
               MESW_PROF(prof[3] += clock64() - tq;)
@@ -769,9 +788,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + (abase_own + aslot) * kAColsPerSlot);
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
               const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
-              mma2_ts(dd, a0, bd, id, f0);
+              if (!(p.dbg & 2)) {
+                mma2_ts(dd, a0, bd, id, f0);
 #pragma unroll
-              for (int j = 1; j < 8; ++j) mma2_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
+                for (int j = 1; j < 8; ++j) mma2_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
+              }
               tc2_commit(&S.aempty[abase_own + aslot]);
               if (++aslot == na_own) { aslot = 0; aph ^= 1; }
               MESW_PROF(prof[4] += clock64() - tq;)
@@ -817,43 +838,49 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           mbar_wait(&S.cfull[sc], pc);
           MESW_PROF(dprof[0] += clock64() - dq;)
           const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
-          for (int q = sg0; q < sg1; ++q) {
+          for (int q = sg0; q < ((p.dbg & 16) ? sg0 : sg1); ++q) {
             const int iss = (q + s0) % p.n_iss;
             const int k = iss == 0 ? kc0 : (iss == 1 ? kc1 : kc2);
             if (iss == 0) ++kc0; else if (iss == 1) ++kc1; else ++kc2;
-            if ((k & 1) != grp) continue;
+            // both groups take part in every job: group g expands k-half g (64 inputs)
             const int na = p.a_na[iss];
             const int aslot = p.a_base[iss] + k % na;
             const int use = k / na;
-            uint32_t cw[2 * WPK];
+            uint32_t cw[WPK];
             const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-              for (int v = 0; v < CHB / 16; ++v) {
-                const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
-                const int w0 = kh * WPK + 4 * v;
-                cw[w0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
-              }
+            for (int v = 0; v < CHB / 16; ++v) {
+              const uint4 t4 = lds128(cb + ((size_t)grp * 128 + mrow) * CHB + v * 16);
+              cw[4 * v] = t4.x; cw[4 * v + 1] = t4.y; cw[4 * v + 2] = t4.z; cw[4 * v + 3] = t4.w;
+            }
             MESW_PROF(dq = clock64();)
             if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
             MESW_PROF(dprof[1] += clock64() - dq;)
             MESW_PROF(dq = clock64();)
             const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
-#pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {
+            {
               uint32_t r[32];
-              dequant_chunk<DB>(&cw[kh * WPK], r);
-              tmem_st32(a0 + lane_addr + 32 * kh, r);
+              if (p.dbg & 1) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) r[i] = cw[i % WPK];
+              } else {
+                dequant_chunk<DB>(cw, r);
+              }
+              if (!(p.dbg & 4)) tmem_st32(a0 + lane_addr + 32 * grp, r);
             }
             MESW_PROF(dprof[2] += clock64() - dq;)
             MESW_PROF(dq = clock64();)
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {  // 4 warps of each CTA -> leader's afull (8 arrivals)
-              if (rank == 0) mbar_arrive(&S.afull[aslot]);
-              else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
+            if (lane == 0) {  // 8 warps of each CTA -> leader's afull (16 arrivals)
+              if (p.dbg & 64) {  // timing probe: leader arrives for both CTAs, peer stays local
+                if (rank == 0) { mbar_arrive(&S.afull[aslot]); mbar_arrive(&S.afull[aslot]); }
+              } else if (rank == 0) {
+                mbar_arrive(&S.afull[aslot]);
+              } else {
+                mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
+              }
             }
             MESW_PROF(dprof[3] += clock64() - dq;)
             MESW_PROF(dprof[7]++;)
@@ -1134,34 +1161,25 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   p.cbytes = p.segs_per_chunk * CB;
   const size_t budget = 232448 - ring_offset();
   // ring depths: prefer (x 3, codes 3, weights >= 3); shrink x/codes first when rows are many
-  // Ring depths: one producer thread walks the rings in unit order, so every ring gets the
-  // same lookahead D (units); D is the largest that fits (<= kMaxStages, >= 2).
-  for (;;) {
-    const size_t per_unit = (a->w ? (size_t)kUnitWBytes : 0) + (size_t)p.xbytes + (size_t)p.n_chunks * p.cbytes;
-    int D = (int)((budget - 1024) / per_unit);
-    if (D > kMaxStages) D = kMaxStages;
-    if (D >= 2) {
-      p.nx = D;
-      p.nw = a->w ? D : 0;
-      p.nc = std::min(kMaxCStages, D * p.n_chunks);
-      break;
+  // Ring depths: activations and codes 3 units ahead (their own producer thread), the
+  // weight ring gets the rest of shared memory (its producer streams independently).
+  {
+    bool ok = false;
+    for (int depth = 3; depth >= 1 && !ok; --depth) {  // code-chunk lookahead in units
+      for (int pass = 0; pass < 8 && !ok; ++pass) {
+        p.nx = depth >= 2 ? 3 : 2;
+        p.nc = std::min(kMaxCStages, depth * p.n_chunks);
+        if (p.n_chunks > 0 && p.nc < 2) p.nc = 2;
+        const size_t used = (size_t)p.nx * p.xbytes + (size_t)p.nc * p.cbytes + 1024;
+        p.nw = a->w ? (int)std::min<size_t>(kMaxStages, budget > used ? (budget - used) / kUnitWBytes : 0) : 0;
+        if (!a->w || p.nw >= (depth >= 2 ? 3 : 2)) { ok = true; break; }
+        if (p.segs_per_chunk <= kDqGroups) break;
+        p.segs_per_chunk = (p.segs_per_chunk / 2 + kDqGroups - 1) / kDqGroups * kDqGroups;  // smaller chunks
+        p.n_chunks = (p.n_seg + p.segs_per_chunk - 1) / p.segs_per_chunk;
+        p.cbytes = p.segs_per_chunk * CB;
+      }
     }
-    // code-heavy launches: two units of weights / activations, the code ring gets the rest
-    const size_t wx = 2 * ((a->w ? (size_t)kUnitWBytes : 0) + (size_t)p.xbytes) + 1024;
-    const int nc = budget > wx ? (int)std::min<size_t>(kMaxCStages, (budget - wx) / p.cbytes) : 0;
-    if (nc >= 2) {
-      p.nx = 2;
-      p.nw = a->w ? 2 : 0;
-      p.nc = nc;
-      break;
-    }
-    if (p.segs_per_chunk > kDqGroups) {  // smaller code chunks
-      p.segs_per_chunk = (p.segs_per_chunk / 2 + kDqGroups - 1) / kDqGroups * kDqGroups;
-      p.n_chunks = (p.n_seg + p.segs_per_chunk - 1) / p.segs_per_chunk;
-      p.cbytes = p.segs_per_chunk * CB;
-      continue;
-    }
-    return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory: fewer than 2 pipeline stages");
+    if (!ok) return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory: fewer than 2 weight stages");
   }
   p.xo = 0;
   p.co = p.nx * p.xbytes;
@@ -1179,7 +1197,8 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
     if (getenv("MESW_ISS")) want = std::min(want, atoi(getenv("MESW_ISS")));
     want = std::max(1, std::min(want, kMaxIssuers));
     bool done = false;
-    for (int n_acc = 2; n_acc >= 1 && !done; --n_acc) {
+    const int nacc_max = getenv("MESW_NACC") ? atoi(getenv("MESW_NACC")) : 2;
+    for (int n_acc = nacc_max; n_acc >= 1 && !done; --n_acc) {
       for (int iss = want; iss >= 1 && !done; --iss) {
         int n_delta = 0;  // issuers that own at least one segment
         for (int i = 0; i < iss; ++i) {
@@ -1190,18 +1209,20 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
         const int cols = kTmemCols - n_acc * 2 * p.NP;
         int slots = cols / kAColsPerSlot;
         if (slots > kMaxASlots) slots = kMaxASlots;
-        if (cols < 0 || (n_delta > 0 && slots < 2 * n_delta)) continue;
-        const int per = n_delta > 0 ? (slots / n_delta) & ~1 : 0;
-        int base = 0;
-        for (int i = 0; i < 3; ++i) { p.a_base[i] = 0; p.a_na[i] = 0; }
-        for (int i = 0; i < iss; ++i) {
-          bool any = false;
-          for (int q = 0; q < p.n_seg; ++q) any |= ((q + (p.w ? 1 : 0)) % iss == i);
-          if (!any) continue;
-          p.a_base[i] = base;
-          p.a_na[i] = per;
-          base += per;
+        if (cols < 0 || slots < n_delta) continue;
+        // every issuer with delta jobs gets >= 1 slot; the rest go to the most loaded
+        int jobs[3] = {0, 0, 0};
+        for (int q = 0; q < p.n_seg; ++q) jobs[(q + (p.w ? 1 : 0)) % iss]++;
+        for (int i = 0; i < 3; ++i) { p.a_base[i] = 0; p.a_na[i] = (i < iss && jobs[i] > 0) ? 1 : 0; }
+        for (int left = slots - n_delta; left > 0; --left) {
+          int best = -1;
+          for (int i = 0; i < iss; ++i)
+            if (jobs[i] > 0 && (best < 0 || jobs[i] * p.a_na[best] > jobs[best] * p.a_na[i])) best = i;
+          if (best < 0) break;
+          p.a_na[best]++;
         }
+        int base = 0;
+        for (int i = 0; i < 3; ++i) { p.a_base[i] = base; base += p.a_na[i]; }
         p.n_acc = n_acc;
         p.n_iss = iss;
         p.n_aslots = base;
