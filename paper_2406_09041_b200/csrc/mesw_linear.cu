@@ -164,6 +164,31 @@ __device__ __forceinline__ void mma2_ts(uint32_t d, uint32_t a_tmem, uint64_t b,
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// Whole-warp issue (all 32 lanes run the issuer loop with warp-uniform operands; one elected
+// lane executes the tcgen05 op).  Issuing from a single divergent lane makes the compiler
+// move every operand to uniform registers through an R2UR.BROADCAST loop per instruction,
+// which doubles the issue cost (tools/micro/tc2_rate.cu: 730 -> 341 cycles per 8 MMAs).
+__device__ __forceinline__ void mma2_ss_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma2_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc2_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 // Commit the issuing thread's MMAs to the same-offset mbarrier in both CTAs of the pair.
 __device__ __forceinline__ void tc2_commit(uint64_t* bar) {
   asm volatile(
@@ -718,8 +743,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           }
         }
       }
-    } else if (lane == 0 && role < p.n_iss) {
-      // ===================== leader: issue the pair's MMAs =====================
+    } else if (role < p.n_iss) {
+      // ===================== leader: issue the pair's MMAs (whole warp, elected lane) ========
       // MMA streams (the base tile, then one per segment) are dealt round-robin to the
       // issuers: stream s -> issuer s % n_iss.  Each accumulator range is owned by exactly
       // one issuer, so its k-ordered accumulate chain stays in one thread's issue order.
@@ -767,11 +792,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             tc_fence_after();
             const uint64_t wd = wdesc0 + (uint64_t)(sw * wstride);
             if (!(p.dbg & 8)) {
-              mma2_ss(d_base, wd, xd, id_base, f0);
+              mma2_ss_w(d_base, wd, xd, id_base, f0);
 #pragma unroll
-              for (int j = 1; j < 8; ++j) mma2_ss(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
+              for (int j = 1; j < 8; ++j) mma2_ss_w(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
             }
-            tc2_commit(&S.wempty[sw]);
+            tc2_commit_w(&S.wempty[sw]);
             if (++sw == p.nw) { sw = 0; pw ^= 1; }
             MESW_PROF(prof[2] += clock64() - tq;)
           }
@@ -789,29 +814,29 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
               const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
               if (!(p.dbg & 2)) {
-                mma2_ts(dd, a0, bd, id, f0);
+                mma2_ts_w(dd, a0, bd, id, f0);
 #pragma unroll
-                for (int j = 1; j < 8; ++j) mma2_ts(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
+                for (int j = 1; j < 8; ++j) mma2_ts_w(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
               }
-              tc2_commit(&S.aempty[abase_own + aslot]);
+              tc2_commit_w(&S.aempty[abase_own + aslot]);
               if (++aslot == na_own) { aslot = 0; aph ^= 1; }
               MESW_PROF(prof[4] += clock64() - tq;)
               MESW_PROF(prof[7]++;)
             }
           }
-          tc2_commit(&S.xempty[sx]);
+          tc2_commit_w(&S.xempty[sx]);
           if (++sx == p.nx) { sx = 0; px ^= 1; }
           if (piece_last) {
-            tc2_commit(&S.accfull[ab]);
+            tc2_commit_w(&S.accfull[ab]);
             if (ab) ++use1; else ++use0;
             if (p.n_acc == 2) ab ^= 1;
           }
           MESW_PROF(prof[5] += clock64() - tu;)
         }
       }
-      if (role == 0) MESW_STAMP(3);
+      if (role == 0 && lane == 0) MESW_STAMP(3);
       MESW_PROF(prof[6] = clock64() - tstart;)
-      MESW_PROF(if (p.tbuf) for (int i = 0; i < 8; ++i) p.tbuf[(role < 2 ? 4096 * 8 + (size_t)blockIdx.x * 16 + role * 8 : 4096 * 48 + (size_t)blockIdx.x * 8) + i] = prof[i];)
+      MESW_PROF(if (p.tbuf && lane == 0) for (int i = 0; i < 8; ++i) p.tbuf[(role < 2 ? 4096 * 8 + (size_t)blockIdx.x * 16 + role * 8 : 4096 * 48 + (size_t)blockIdx.x * 8) + i] = prof[i];)
     }
   } else if (warp < kEpiWarp0) {
     // ===================== dequant groups: own codes -> own TMEM A rows =====================
@@ -874,13 +899,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {  // 8 warps of each CTA -> leader's afull (16 arrivals)
-              if (p.dbg & 64) {  // timing probe: leader arrives for both CTAs, peer stays local
-                if (rank == 0) { mbar_arrive(&S.afull[aslot]); mbar_arrive(&S.afull[aslot]); }
-              } else if (rank == 0) {
-                mbar_arrive(&S.afull[aslot]);
-              } else {
-                mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
-              }
+              if (rank == 0) mbar_arrive(&S.afull[aslot]);
+              else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
             }
             MESW_PROF(dprof[3] += clock64() - dq;)
             MESW_PROF(dprof[7]++;)
@@ -1165,9 +1185,10 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   // weight ring gets the rest of shared memory (its producer streams independently).
   {
     bool ok = false;
-    for (int depth = 3; depth >= 1 && !ok; --depth) {  // code-chunk lookahead in units
+    const int d0 = getenv("MESW_CDEPTH") ? atoi(getenv("MESW_CDEPTH")) : 3;
+    for (int depth = d0; depth >= 1 && !ok; --depth) {  // code-chunk lookahead in units
       for (int pass = 0; pass < 8 && !ok; ++pass) {
-        p.nx = depth >= 2 ? 3 : 2;
+        p.nx = getenv("MESW_NX") ? atoi(getenv("MESW_NX")) : (depth >= 2 ? 3 : 2);
         p.nc = std::min(kMaxCStages, depth * p.n_chunks);
         if (p.n_chunks > 0 && p.nc < 2) p.nc = 2;
         const size_t used = (size_t)p.nx * p.xbytes + (size_t)p.nc * p.cbytes + 1024;

@@ -20,6 +20,20 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 template <int CG>
+__device__ __forceinline__ void mma_ss_el(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  if (CG == 2)
+    asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
+  else
+    asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+template <int CG>
+__device__ __forceinline__ void mma_ts_el(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  if (CG == 2)
+    asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
+  else
+    asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
+}
+template <int CG>
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
   if (CG == 2)
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
@@ -57,7 +71,37 @@ __global__ void bench(int N, int R, int nis, int ts, unsigned long long* out, in
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t t = tb;
   const int M = CG == 2 ? 256 : 128;
-  if (rank == 0 && warp >= 1 && warp <= nis && (threadIdx.x & 31) == 0) {
+  if (ts >= 4 && rank == 0 && warp >= 1 && warp <= nis) {
+    const uint32_t a = sa(sm) + (warp - 1) * 16384, b = sa(sm + 65536) + (warp - 1) * 16384;
+    const uint32_t id = idesc(M, N);
+    const uint64_t da = sdesc(a), db = sdesc(b);
+    const uint32_t d = t + (warp - 1) * 64;
+    const uint32_t at = t + 256 + (warp - 1) * 64;
+    long long c0 = clock64();
+    for (int i = 0; i < R; i += 8) {
+      if (ts == 4) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mma_ts_el<CG>(d, at + 8 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mma_ss_el<CG>(d, da + 16 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+      }
+      if (CG == 2)
+        asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(sa(&dummy)), "h"((uint16_t)3));
+      else
+        asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(sa(&dummy)));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (CG == 2)
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(sa(&bar)), "h"((uint16_t)3));
+      else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(&bar)));
+      long long c1 = clock64();
+      asm volatile("{\n.reg .pred P1;\nWE:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra WE;\n}\n" ::"r"(sa(&bar)));
+      long long c2 = clock64();
+      if (warp == 1 && blockIdx.x == 0) { out[0] = c1 - c0; out[1] = c2 - c0; }
+    }
+  } else if (rank == 0 && warp >= 1 && warp <= nis && (threadIdx.x & 31) == 0) {
     const uint32_t a = sa(sm) + (warp - 1) * 16384, b = sa(sm + 65536) + (warp - 1) * 16384;
     const uint32_t id = idesc(M, N);
     const uint64_t da = sdesc(a), db = sdesc(b);
@@ -65,7 +109,10 @@ __global__ void bench(int N, int R, int nis, int ts, unsigned long long* out, in
     const uint32_t at = t + 256 + (warp - 1) * 64; // TMEM A operands: cols [256, 448)
     long long c0 = clock64();
     for (int i = 0; i < R; i += 8) {
-      if (ts) {
+      if (ts == 3 && warp == 1) {  // mixed: warp 1 SS (base-like), others TS (delta-like)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mma_ss<CG>(d, da + 16 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
+      } else if (ts) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) mma_ts<CG>(d, at + 8 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
       } else if (ts == 0) {
@@ -107,13 +154,11 @@ int main() {
   const int R = 4096;
   cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
-  // ts: 0 SS, 1 TS, 2 no MMAs (commits only); cmode commits per 8-MMA group
-  for (int ts = 0; ts < 3; ++ts)
-    for (int cg = 1; cg <= 2; ++cg)
-      for (int nis = 1; nis <= 3; nis += 2)
-        for (int cmode : {0, 1, 3}) {
-          if (ts == 2 && cmode == 0) continue;
-          const int N = 48;
+  for (int ts : {0, 1, 4, 5})
+    for (int cg = 2; cg <= 2; ++cg)
+      for (int nis = 1; nis <= 3; ++nis)
+        for (int N : {16, 48}) {
+          const int cmode = 1;
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3(cg == 2 ? 2 : 1);
           cfg.blockDim = dim3(128);
@@ -127,8 +172,8 @@ int main() {
           if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return 1; }
           unsigned long long h[2];
           cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-          printf("%s cta_group::%d issuers %d commits/8mma %d: issue %7.1f cyc per 8-group, complete %7.1f\n",
-                 ts == 2 ? "none" : (ts ? "TS" : "SS"), cg, nis, cmode, (double)h[0] / (R / 8), (double)h[1] / (R / 8));
+          printf("%s cta_group::%d issuers %d N=%2d (+1 commit/8): %7.1f cyc per 8-MMA group per issuer -> aggregate %5.1f cyc/MMA\n",
+                 ts == 3 ? "mixed(SS w1,TS rest)" : ts == 4 ? "TS-warp" : ts == 5 ? "SS-warp" : (ts ? "TS" : "SS"), cg, nis, N, (double)h[1] / (R / 8), (double)h[1] / R / nis);
         }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
