@@ -32,10 +32,10 @@
 
 namespace mesw {
 
-constexpr int kDqGroups = 2;  // dequant warpgroups: group g expands k-half g of every job
-// warp roles: 0 weight-tile producer, 1-2 MMA issuers, 3 code + activation producer, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
-constexpr int kProdWarp = 0, kMmaWarp = 1, kXCProdWarp = 3;
-constexpr int kMaxIssuers = 2;  // warps 1..2
+constexpr int kDqGroups = 2;  // dequant warpgroups: group g fills the A slots with parity g
+// warp roles: 0 producer (codes, weight tiles, activations), 1-3 MMA issuers, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
+constexpr int kProdWarp = 0, kMmaWarp = 1;
+constexpr int kMaxIssuers = 3;  // warps 1..3
 constexpr int kDqWarp0 = 4, kEpiWarp0 = kDqWarp0 + 4 * kDqGroups;
 constexpr int kThreads = (kEpiWarp0 + 4) * 32;  // 16 warps
 constexpr int kTmemCols = 512;
@@ -114,6 +114,7 @@ struct Smem {
   int tok2seg[kMaxRows];
   SegDesc segs[MESW_MAX_SEGMENTS];
   int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
+  int8_t seg_iss[MESW_MAX_SEGMENTS];                         // MMA issuer of each segment
   float xsal[kMaxRows][16];  // x[t][salient idx r] of the current column group (k <= 16 fast path)
 };
 
@@ -377,6 +378,13 @@ struct PieceOrder {
   }
 };
 
+// MMA issuer of expert segment q.  With a base weight, issuer 0 issues ONLY the base tile
+// (so the weight stream never waits on the delta pipeline) and the segments go round-robin
+// to issuers 1..n-1; without one (or with a single issuer) they go round-robin to all.
+__host__ __device__ __forceinline__ int seg_issuer(int q, int n_iss, bool has_w) {
+  return (has_w && n_iss > 1) ? 1 + q % (n_iss - 1) : q % n_iss;
+}
+
 __device__ __forceinline__ int unit_owner(long long u, long long T, int G) {
   return (int)(((u + 1) * (long long)G - 1) / T);
 }
@@ -607,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     for (int i = 0; i < p.nx; ++i) { mbar_init(&S.xfull[i], peer_relay); mbar_init(&S.xempty[i], p.n_iss); }
     for (int i = 0; i < p.nw; ++i) { mbar_init(&S.wfull[i], peer_relay); mbar_init(&S.wempty[i], 1); }
     for (int i = 0; i < p.nc; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 128 * kDqGroups); }
-    for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 16); mbar_init(&S.aempty[i], 1); }
+    for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 8); mbar_init(&S.aempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], p.n_iss); mbar_init(&S.accempty[i], 8); }
     mbar_init(&S.finbar, 1);
     fence_mbar_init();
@@ -634,6 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     d.winN = ((d.end + 15) & ~15) - d.begin;   // 16-token window(s)
     S.segs[q] = d;
     for (int t = d.begin; t < d.end; ++t) S.tok2seg[t] = q;
+    S.seg_iss[q] = (int8_t)seg_issuer(q, p.n_iss, p.w != nullptr);
   }
   tc_fence_before();
   __syncthreads();
@@ -644,80 +653,68 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   if (threadIdx.x == 0) MESW_STAMP(0);
   pdl_trigger();
 
-  if (warp == kProdWarp || warp == kXCProdWarp) {
-    // ===================== producers (own column group / own x half) =====================
-    // warp 0: weight tiles (static: streamed from the first cycle, even before the previous
-    // kernel completes -- PDL); warp 3: per unit the code chunks (static, prefetched before
-    // the PDL wait) and the activation half-tile (after it).  One thread each.
+  if (warp == kProdWarp) {
+    // ===================== producer (own column group / own x half), one thread =====================
+    // per unit: code chunks, weight tile (both static: the first rings' worth is requested
+    // before the PDL wait), activation half-tile (after it).
     if (lane == 0) {
       uint64_t evict_first;  // weights / codes are streamed once: do not let them evict partials
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
-      if (warp == kProdWarp) {
-        int sw = 0;
-        uint32_t pw = 0;
-        bool wfirst = true;
-        for (int pi = 0; pi < (has_w ? po.np : 0); ++pi) {
+      int sw = 0, sx = 0, sc = 0;
+      uint32_t pw = 0, px = 0, pc = 0;
+      bool wfirst = true, xfirst = true, cfirst = true;
+      auto issue_static = [&](int cg, int ks) {
+        const long long unit = (long long)cg * p.n_ks + ks;  // this CTA's unit
+        for (int ch = 0; ch < p.n_chunks; ++ch) {
+          const int sg0 = ch * p.segs_per_chunk;
+          const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
+          if (!cfirst) mbar_wait(&S.cempty[sc], pc ^ 1);
+          if (p.dbg & 32) {
+            mbar_arrive(&S.cfull[sc]);
+          } else {
+            mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
+            for (int q = sg0; q < sg1; ++q)
+              bulk_g2s_hint(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB,
+                            S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[sc], evict_first);
+          }
+          if (++sc == p.nc) { sc = 0; pc ^= 1; cfirst = false; }
+        }
+        if (has_w) {
+          if (!wfirst) mbar_wait(&S.wempty[sw], pw ^ 1);
+          mbar_arrive_expect_tx(&S.wfull[sw], kUnitWBytes);
+          bulk_g2s_hint(ring + p.wo + (size_t)sw * kUnitWBytes, p.w + (size_t)unit * kUnitWBytes, kUnitWBytes,
+                        &S.wfull[sw], evict_first);
+          if (++sw == p.nw) { sw = 0; pw ^= 1; wfirst = false; }
+        }
+      };
+      int n_pre = 0;
+      {
+        int D = p.nx;
+        if (has_w && p.nw < D) D = p.nw;
+        if (p.n_chunks > 0 && p.nc / p.n_chunks < D) D = p.nc / p.n_chunks;
+        for (int pi = 0; pi < po.np && n_pre < D; ++pi) {
           long long pa, pb;
           po.bounds(pi, pa, pb);
           const int cgp = po.cg_of(pi);
-          const int cg = 2 * cgp + (int)rank;
-          for (long long u = pa; u < pb; ++u) {
-            const long long unit = (long long)cg * p.n_ks + (u - (long long)cgp * p.n_ks);
-            if (!wfirst) mbar_wait(&S.wempty[sw], pw ^ 1);
-            mbar_arrive_expect_tx(&S.wfull[sw], kUnitWBytes);
-            bulk_g2s_hint(ring + p.wo + (size_t)sw * kUnitWBytes, p.w + (size_t)unit * kUnitWBytes, kUnitWBytes,
-                          &S.wfull[sw], evict_first);
-            if (++sw == p.nw) { sw = 0; pw ^= 1; wfirst = false; }
-          }
+          for (long long u = pa; u < pb && n_pre < D; ++u, ++n_pre)
+            issue_static(2 * cgp + (int)rank, (int)(u - (long long)cgp * p.n_ks));
         }
-      } else {
-        int sx = 0, sc = 0;
-        uint32_t px = 0, pc = 0;
-        bool xfirst = true, cfirst = true;
-        auto issue_codes = [&](int cg, int ks) {
-          const long long unit = (long long)cg * p.n_ks + ks;  // this CTA's unit
-          for (int ch = 0; ch < p.n_chunks; ++ch) {
-            const int sg0 = ch * p.segs_per_chunk;
-            const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-            if (!cfirst) mbar_wait(&S.cempty[sc], pc ^ 1);
-            if (p.dbg & 32) {
-              mbar_arrive(&S.cfull[sc]);
-            } else {
-              mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
-              for (int q = sg0; q < sg1; ++q)
-                bulk_g2s_hint(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB,
-                              S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[sc], evict_first);
-            }
-            if (++sc == p.nc) { sc = 0; pc ^= 1; cfirst = false; }
-          }
-        };
-        int n_pre = 0;  // units whose codes go out before the PDL wait
-        if (p.n_chunks > 0) {
-          const int D = p.nc / p.n_chunks;
-          for (int pi = 0; pi < po.np && n_pre < D; ++pi) {
-            long long pa, pb;
-            po.bounds(pi, pa, pb);
-            const int cgp = po.cg_of(pi);
-            for (long long u = pa; u < pb && n_pre < D; ++u, ++n_pre)
-              issue_codes(2 * cgp + (int)rank, (int)(u - (long long)cgp * p.n_ks));
-          }
-        }
-        pdl_wait();
-        int idx = 0;
-        for (int pi = 0; pi < po.np; ++pi) {
-          long long pa, pb;
-          po.bounds(pi, pa, pb);
-          const int cgp = po.cg_of(pi);
-          const int cg = 2 * cgp + (int)rank;
-          for (long long u = pa; u < pb; ++u, ++idx) {
-            const int ks = (int)(u - (long long)cgp * p.n_ks);
-            if (idx >= n_pre && p.n_chunks > 0) issue_codes(cg, ks);
-            if (!xfirst) mbar_wait(&S.xempty[sx], px ^ 1);
-            mbar_arrive_expect_tx(&S.xfull[sx], (uint32_t)p.xbytes);
-            bulk_g2s(ring + p.xo + (size_t)sx * p.xbytes,
-                     p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK, p.xbytes, &S.xfull[sx]);
-            if (++sx == p.nx) { sx = 0; px ^= 1; xfirst = false; }
-          }
+      }
+      pdl_wait();
+      int idx = 0;
+      for (int pi = 0; pi < po.np; ++pi) {
+        long long pa, pb;
+        po.bounds(pi, pa, pb);
+        const int cgp = po.cg_of(pi);
+        const int cg = 2 * cgp + (int)rank;
+        for (long long u = pa; u < pb; ++u, ++idx) {
+          const int ks = (int)(u - (long long)cgp * p.n_ks);
+          if (idx >= n_pre) issue_static(cg, ks);
+          if (!xfirst) mbar_wait(&S.xempty[sx], px ^ 1);
+          mbar_arrive_expect_tx(&S.xfull[sx], (uint32_t)p.xbytes);
+          bulk_g2s(ring + p.xo + (size_t)sx * p.xbytes,
+                   p.x + (size_t)ks * NP * kUnitK + (size_t)rank * HP * kUnitK, p.xbytes, &S.xfull[sx]);
+          if (++sx == p.nx) { sx = 0; px ^= 1; xfirst = false; }
         }
       }
     }
@@ -745,10 +742,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       }
     } else if (role < p.n_iss) {
       // ===================== leader: issue the pair's MMAs (whole warp, elected lane) ========
-      // MMA streams (the base tile, then one per segment) are dealt round-robin to the
-      // issuers: stream s -> issuer s % n_iss.  Each accumulator range is owned by exactly
-      // one issuer, so its k-ordered accumulate chain stays in one thread's issue order.
-      const int s0 = has_w ? 1 : 0;  // stream index of segment 0
+      // Issuer 0 owns the base tile, segments go to seg_issuer().  Each accumulator range is
+      // owned by exactly one issuer, so its k-ordered accumulate chain stays in one issue order.
       const bool do_base = has_w && role == 0;
       const uint64_t xdesc0 = smem_desc(smem_u32(ring + p.xo));
       const uint64_t wdesc0 = smem_desc(smem_u32(ring + p.wo));
@@ -763,6 +758,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       int use0 = 0, use1 = 0;
       MESW_PROF(long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
       MESW_PROF(const long long tstart = clock64();)
+      MESW_PROF(int ucount = 0;)
+      MESW_PROF(if (p.tbuf && blockIdx.x == 0 && lane == 0) p.tbuf[4096 * 56 + 256 + role] = tstart;)
       MESW_PROF(long long tq;)
       for (int pi = 0; pi < po.np; ++pi) {
         long long pa, pb;
@@ -801,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             MESW_PROF(prof[2] += clock64() - tq;)
           }
           for (int q = 0; q < p.n_seg; ++q) {
-            if (!(p.dbg & 16) && (q + s0) % p.n_iss == role) {
+            if (!(p.dbg & 16) && S.seg_iss[q] == role) {
               MESW_PROF(tq = clock64();)
               mbar_wait_cluster(&S.afull[abase_own + aslot], aph);
               MESW_PROF(prof[3] += clock64() - tq;)
@@ -832,6 +829,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             if (p.n_acc == 2) ab ^= 1;
           }
           MESW_PROF(prof[5] += clock64() - tu;)
+          MESW_PROF(if (p.tbuf && blockIdx.x == 0 && lane == 0 && ucount < 64) p.tbuf[4096 * 56 + role * 64 + ucount] = clock64();)
+          MESW_PROF(++ucount;)
         }
       }
       if (role == 0 && lane == 0) MESW_STAMP(3);
@@ -847,10 +846,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     constexpr int WPK = CHB / 4;  // code words per k-half of a channel
     int sc = 0;
     uint32_t pc = 0;
-    int kc0 = 0, kc1 = 0, kc2 = 0;  // jobs seen so far per issuer stream
-    const int s0 = p.w != nullptr ? 1 : 0;
+    // per issuer: position in its A sub-ring and completed laps (no divisions in the loop)
+    int ps0 = 0, ps1 = 0, ps2 = 0, us0 = 0, us1 = 0, us2 = 0;
     MESW_PROF(long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
     MESW_PROF(const long long dstart = clock64();)
+    MESW_PROF(int dcount = 0;)
     MESW_PROF(long long dq;)
     for (int pi = 0; pi < (p.n_seg > 0 ? po.np : 0); ++pi) {
       long long pa, pb;
@@ -864,41 +864,51 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           MESW_PROF(dprof[0] += clock64() - dq;)
           const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
           for (int q = sg0; q < ((p.dbg & 16) ? sg0 : sg1); ++q) {
-            const int iss = (q + s0) % p.n_iss;
-            const int k = iss == 0 ? kc0 : (iss == 1 ? kc1 : kc2);
-            if (iss == 0) ++kc0; else if (iss == 1) ++kc1; else ++kc2;
-            // both groups take part in every job: group g expands k-half g (64 inputs)
-            const int na = p.a_na[iss];
-            const int aslot = p.a_base[iss] + k % na;
-            const int use = k / na;
-            uint32_t cw[WPK];
+            const int iss = S.seg_iss[q];
+            const int pos = iss == 0 ? ps0 : (iss == 1 ? ps1 : ps2);
+            const int use = iss == 0 ? us0 : (iss == 1 ? us1 : us2);
+            {
+              const bool wrap = pos + 1 == p.a_na[iss];
+              const int np1 = wrap ? 0 : pos + 1, nu = use + (wrap ? 1 : 0);
+              if (iss == 0) { ps0 = np1; us0 = nu; } else if (iss == 1) { ps1 = np1; us1 = nu; } else { ps2 = np1; us2 = nu; }
+            }
+            // slot-affine groups: A slot s is always filled by group s % 2 (whole jobs, both
+            // k-halves: two independent dequant chains per thread), so every slot is written
+            // by one group and read by one issuer, in sequence
+            const int aslot = p.a_base[iss] + pos;
+            if ((aslot & 1) != grp) continue;
+            uint32_t cw[2 * WPK];
             const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
 #pragma unroll
-            for (int v = 0; v < CHB / 16; ++v) {
-              const uint4 t4 = lds128(cb + ((size_t)grp * 128 + mrow) * CHB + v * 16);
-              cw[4 * v] = t4.x; cw[4 * v + 1] = t4.y; cw[4 * v + 2] = t4.z; cw[4 * v + 3] = t4.w;
-            }
+            for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+              for (int v = 0; v < CHB / 16; ++v) {
+                const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
+                const int w0 = kh * WPK + 4 * v;
+                cw[w0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
+              }
             MESW_PROF(dq = clock64();)
             if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
             MESW_PROF(dprof[1] += clock64() - dq;)
             MESW_PROF(dq = clock64();)
             const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
-            {
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
               uint32_t r[32];
               if (p.dbg & 1) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) r[i] = cw[i % WPK];
+                for (int i = 0; i < 32; ++i) r[i] = cw[kh * WPK + i % WPK];
               } else {
-                dequant_chunk<DB>(cw, r);
+                dequant_chunk<DB>(&cw[kh * WPK], r);
               }
-              if (!(p.dbg & 4)) tmem_st32(a0 + lane_addr + 32 * grp, r);
+              if (!(p.dbg & 4)) tmem_st32(a0 + lane_addr + 32 * kh, r);
             }
             MESW_PROF(dprof[2] += clock64() - dq;)
             MESW_PROF(dq = clock64();)
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {  // 8 warps of each CTA -> leader's afull (16 arrivals)
+            if (lane == 0) {  // the group's 4 warps of each CTA -> leader's afull (8 arrivals)
               if (rank == 0) mbar_arrive(&S.afull[aslot]);
               else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
             }
@@ -907,6 +917,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           }
           mbar_arrive(&S.cempty[sc]);  // every thread: release orders its own smem reads
           if (++sc == p.nc) { sc = 0; pc ^= 1; }
+          MESW_PROF(if (p.tbuf && blockIdx.x == 0 && threadIdx.x == kDqWarp0 * 32 + grp * 128 && dcount < 64) p.tbuf[4096 * 56 + 128 + grp * 64 + dcount] = clock64();)
+          MESW_PROF(++dcount;)
         }
       }
     }
@@ -1105,7 +1117,7 @@ static unsigned long long* g_tbuf = nullptr;
 // Debug: copy the last MESW_TIMING launch's per-CTA globaltimer stamps (8 per CTA).
 extern "C" int mesw_debug_timing_copy(unsigned long long* h_out, int n_ctas) {
   if (!g_tbuf) return mesw_fail(MESW_ERR_VALUE, "no timing buffer (set MESW_TIMING)");
-  cudaError_t e = cudaMemcpy(h_out, g_tbuf, (size_t)56 * 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpy(h_out, g_tbuf, (size_t)60 * 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? MESW_OK : mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
 }
 
@@ -1161,7 +1173,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
     const char* e = getenv("MESW_DBG");
     p.dbg = e ? atoi(e) : 0;
     if (getenv("MESW_TIMING")) {
-      if (!g_tbuf) cudaMalloc(&g_tbuf, 56 * 4096 * sizeof(unsigned long long)); cudaMemset(g_tbuf, 0, 56 * 4096 * 8);
+      if (!g_tbuf) cudaMalloc(&g_tbuf, 60 * 4096 * sizeof(unsigned long long)); cudaMemset(g_tbuf, 0, 60 * 4096 * 8);
       p.tbuf = g_tbuf;
     }
   }
@@ -1183,24 +1195,23 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   // ring depths: prefer (x 3, codes 3, weights >= 3); shrink x/codes first when rows are many
   // Ring depths: activations and codes 3 units ahead (their own producer thread), the
   // weight ring gets the rest of shared memory (its producer streams independently).
-  {
-    bool ok = false;
-    const int d0 = getenv("MESW_CDEPTH") ? atoi(getenv("MESW_CDEPTH")) : 3;
-    for (int depth = d0; depth >= 1 && !ok; --depth) {  // code-chunk lookahead in units
-      for (int pass = 0; pass < 8 && !ok; ++pass) {
-        p.nx = getenv("MESW_NX") ? atoi(getenv("MESW_NX")) : (depth >= 2 ? 3 : 2);
-        p.nc = std::min(kMaxCStages, depth * p.n_chunks);
-        if (p.n_chunks > 0 && p.nc < 2) p.nc = 2;
-        const size_t used = (size_t)p.nx * p.xbytes + (size_t)p.nc * p.cbytes + 1024;
-        p.nw = a->w ? (int)std::min<size_t>(kMaxStages, budget > used ? (budget - used) / kUnitWBytes : 0) : 0;
-        if (!a->w || p.nw >= (depth >= 2 ? 3 : 2)) { ok = true; break; }
-        if (p.segs_per_chunk <= kDqGroups) break;
-        p.segs_per_chunk = (p.segs_per_chunk / 2 + kDqGroups - 1) / kDqGroups * kDqGroups;  // smaller chunks
-        p.n_chunks = (p.n_seg + p.segs_per_chunk - 1) / p.segs_per_chunk;
-        p.cbytes = p.segs_per_chunk * CB;
-      }
+  // Ring depths: the producer walks all rings in unit order, so they share one lookahead D
+  // (units), the largest that fits (<= kMaxStages, codes ring <= kMaxCStages chunks).
+  for (;;) {
+    const size_t per_unit = (a->w ? (size_t)kUnitWBytes : 0) + (size_t)p.xbytes + (size_t)p.n_chunks * p.cbytes;
+    int D = (int)((budget - 1024) / per_unit);
+    if (D > kMaxStages) D = kMaxStages;
+    if (p.n_chunks > 0 && D * p.n_chunks > kMaxCStages) D = kMaxCStages / p.n_chunks;
+    if (D >= 2) {
+      p.nx = D;
+      p.nw = a->w ? D : 0;
+      p.nc = D * p.n_chunks;
+      break;
     }
-    if (!ok) return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory: fewer than 2 weight stages");
+    if (p.segs_per_chunk <= kDqGroups) return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory: fewer than 2 stages");
+    p.segs_per_chunk = (p.segs_per_chunk / 2 + kDqGroups - 1) / kDqGroups * kDqGroups;  // smaller chunks
+    p.n_chunks = (p.n_seg + p.segs_per_chunk - 1) / p.segs_per_chunk;
+    p.cbytes = p.segs_per_chunk * CB;
   }
   p.xo = 0;
   p.co = p.nx * p.xbytes;
@@ -1210,9 +1221,9 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   smem = 232448;  // one CTA per SM regardless: the slack stages the final stream-K reduction
   p.ring_bytes = (int)(smem - ring_offset());
   // TMEM: n_acc buffers of [D_base NP | D_delta NP] columns, then the A ring (64-col job slots)
-  // MMA issuers: streams (base tile, then one per segment) dealt round-robin.  Each issuer
-  // with delta jobs needs its own even A sub-ring (>= 2 slots of 64 TMEM columns); prefer
-  // two accumulator buffers, then more issuers.
+  // MMA issuers (seg_issuer): the base tile on issuer 0, segments on the others.  Each
+  // issuer with delta jobs owns an A sub-ring (>= 1 slot of 64 TMEM columns); prefer two
+  // accumulator buffers, then more issuers.
   {
     int want = (p.w ? 1 : 0) + p.n_seg;
     if (getenv("MESW_ISS")) want = std::min(want, atoi(getenv("MESW_ISS")));
@@ -1224,7 +1235,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
         int n_delta = 0;  // issuers that own at least one segment
         for (int i = 0; i < iss; ++i) {
           bool any = false;
-          for (int q = 0; q < p.n_seg; ++q) any |= ((q + (p.w ? 1 : 0)) % iss == i);
+          for (int q = 0; q < p.n_seg; ++q) any |= (seg_issuer(q, iss, p.w != nullptr) == i);
           n_delta += any ? 1 : 0;
         }
         const int cols = kTmemCols - n_acc * 2 * p.NP;
@@ -1233,7 +1244,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
         if (cols < 0 || slots < n_delta) continue;
         // every issuer with delta jobs gets >= 1 slot; the rest go to the most loaded
         int jobs[3] = {0, 0, 0};
-        for (int q = 0; q < p.n_seg; ++q) jobs[(q + (p.w ? 1 : 0)) % iss]++;
+        for (int q = 0; q < p.n_seg; ++q) jobs[seg_issuer(q, iss, p.w != nullptr)]++;
         for (int i = 0; i < 3; ++i) { p.a_base[i] = 0; p.a_na[i] = (i < iss && jobs[i] > 0) ? 1 : 0; }
         for (int left = slots - n_delta; left > 0; --left) {
           int best = -1;

@@ -21,7 +21,7 @@ torch.cuda.synchronize()
 plan(); torch.cuda.synchronize()
 G = min(148, (n // 128) * (m // 128))
 G -= G % 2
-buf = np.zeros(56 * 4096, np.uint64)
+buf = np.zeros(60 * 4096, np.uint64)
 _lib.check(L.mesw_debug_timing_copy(buf.ctypes.data, G))
 t = buf[:G * 8].reshape(G, 8).astype(np.int64)
 prof = buf[4096 * 8:4096 * 8 + G * 16].reshape(G, 2, 8).astype(np.int64)
@@ -48,3 +48,11 @@ for g in range(2):
 eprof = buf[4096 * 40:4096 * 40 + G * 16].reshape(G, 16).astype(np.int64)
 sel = eprof[:, 0] > 0
 print("  final red (cycles):", " ".join(f"{n}={np.median(eprof[sel, i]):.0f}/{np.max(eprof[sel, i]):.0f}" for i, n in enumerate(["prefetch_issue", "stage_wait", "reduce+store", "ncontrib"])), f"n={sel.sum()}")
+tl = buf[4096 * 56:4096 * 56 + 260].astype(np.int64)
+t0c = tl[256]
+if t0c:
+    for nm, off in (("issuer0 unit ends", 0), ("issuer1 unit ends", 64), ("deq grp0 chunk ends", 128), ("deq grp1 chunk ends", 192)):
+        v = tl[off:off + 64]
+        v = v[v > 0]
+        if v.size:
+            print(f"  {nm:22s}", " ".join(f"{(x - t0c):6d}" for x in v[:30]))

@@ -34,6 +34,10 @@ __device__ __forceinline__ void mma_ts_el(uint32_t d, uint32_t a, uint64_t b, ui
     asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
 }
 template <int CG>
+__device__ __forceinline__ void mma_ts_i8_el(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
+}
+template <int CG>
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
   if (CG == 2)
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc));
@@ -79,7 +83,11 @@ __global__ void bench(int N, int R, int nis, int ts, unsigned long long* out, in
     const uint32_t at = t + 256 + (warp - 1) * 64;
     long long c0 = clock64();
     for (int i = 0; i < R; i += 8) {
-      if (ts == 4) {
+      if (ts == 6) {  // int8 TS: 4 MMAs of K=32 per 128-wide k-step; idesc D s32, A/B s8
+        const uint32_t idi = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mma_ts_i8_el<CG>(d, at + 8 * j, db + 16 * j, idi, (i | j) ? 1u : 0u);
+      } else if (ts == 4) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) mma_ts_el<CG>(d, at + 8 * j, db + 16 * j, id, (i | j) ? 1u : 0u);
       } else {
@@ -154,7 +162,7 @@ int main() {
   const int R = 4096;
   cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
-  for (int ts : {0, 1, 4, 5})
+  for (int ts : {4, 6})
     for (int cg = 2; cg <= 2; ++cg)
       for (int nis = 1; nis <= 3; ++nis)
         for (int N : {16, 48}) {
@@ -173,7 +181,7 @@ int main() {
           unsigned long long h[2];
           cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
           printf("%s cta_group::%d issuers %d N=%2d (+1 commit/8): %7.1f cyc per 8-MMA group per issuer -> aggregate %5.1f cyc/MMA\n",
-                 ts == 3 ? "mixed(SS w1,TS rest)" : ts == 4 ? "TS-warp" : ts == 5 ? "SS-warp" : (ts ? "TS" : "SS"), cg, nis, N, (double)h[1] / (R / 8), (double)h[1] / R / nis);
+                 ts == 3 ? "mixed(SS w1,TS rest)" : ts == 4 ? "TS-warp" : ts == 6 ? "TS-i8-warp(4 MMA/kstep)" : ts == 5 ? "SS-warp" : (ts ? "TS" : "SS"), cg, nis, N, (double)h[1] / (R / 8), (double)h[1] / R / nis);
         }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
