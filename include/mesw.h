@@ -212,11 +212,14 @@ int mesw_rmsnorm(const uint16_t* d_x, int ldx, const uint16_t* d_w, int B, int H
 int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_pos, int B, int n_heads,
                      int n_kv, int head_dim, float theta, uint16_t* d_kcache,
                      uint16_t* d_vcache, int ctx_max, void* stream);
-/* GQA decode attention over len[b] cached positions; out [B][n_heads*head_dim]. */
+/* GQA decode attention over len[b] cached positions; out [B][n_heads*head_dim].
+ * Split over the context in 64-position blocks (partials in `workspace`, then merged);
+ * workspace >= mesw_attention_workspace_bytes(B, n_heads, ctx_max). head_dim 128. */
+uint64_t mesw_attention_workspace_bytes(int B, int n_heads, int ctx_max);
 int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
                           const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
                           int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
-                          int out_np, void* stream);
+                          int out_np, void* workspace, uint64_t workspace_bytes, void* stream);
 /* out = silu(gate) * up for rows [gate(I) | up(I)]. */
 int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,
                 int out_np, void* stream);

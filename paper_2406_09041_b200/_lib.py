@@ -75,9 +75,10 @@ _SIGNATURES = [
                                C.c_int, C.c_int, C.c_void_p]),
     ("mesw_rope_append", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_float, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    ("mesw_attention_workspace_bytes", C.c_uint64, [C.c_int, C.c_int, C.c_int]),
     ("mesw_attention_decode", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                         C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
-                                        C.c_void_p]),
+                                        C.c_void_p, C.c_uint64, C.c_void_p]),
     ("mesw_swiglu", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
                               C.c_void_p]),
     ("mesw_argmax", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),

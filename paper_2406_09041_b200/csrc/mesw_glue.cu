@@ -153,118 +153,121 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int ld_qkv, const
 //   scores: thread t owns position t (all G heads, 128-dim dot from smem),
 //   softmax: block reductions per head (fixed order),
 //   P.V: thread = (4-dim group, position slice), slices reduced through smem.
-// D must be 128; L <= kAttnMaxCtx.
-constexpr int kAttnThreads = 256;
-constexpr int kAttnMaxCtx = 320;
-constexpr int kAttnRow = 136;  // bf16 per staged row (128 + 8 pad)
+// GQA decode attention, split over the context (flash-decoding): CTA (b, kv head g, split s)
+// handles positions [64 s, 64 s + 64) for the G query heads of kv head g and writes a
+// partial (running max, sum of exponentials, unnormalised output) per head; a second
+// kernel merges the splits.  Many small CTAs stream the KV cache at full occupancy
+// (the cache is read once per step: an HBM-bound pass).  D must be 128.
+constexpr int kAttnThreads = 128;
+constexpr int kAttnSplit = 64;     // positions per CTA
+constexpr int kAttnRow = 136;      // bf16 per staged row (128 + 8 pad: conflict-free row reads)
+constexpr int kAttnPart = 2 + 128; // floats per (b, head, split) partial: m, l, o[128]
 
 template <int G>
-__global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(
+__global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
     const uint16_t* __restrict__ q, int ld_q, const uint16_t* __restrict__ kc, const uint16_t* __restrict__ vc,
-    const int32_t* __restrict__ len, int n_kv, int ctx_max, float scale, uint16_t* __restrict__ out, int ld_out,
-    int out_np) {
+    const int32_t* __restrict__ len, int n_kv, int ctx_max, float scale, float* __restrict__ part, int S) {
   pdl_trigger();
   pdl_wait();  // inputs may come from the previous kernel in the stream
   constexpr int D = 128;
-  extern __shared__ __align__(16) uint8_t smraw[];
-  uint16_t* Ks = reinterpret_cast<uint16_t*>(smraw);                  // [L][136]
-  uint16_t* Vs = Ks + (size_t)kAttnMaxCtx * kAttnRow;                 // [L][136]
-  float* qs = reinterpret_cast<float*>(Vs + (size_t)kAttnMaxCtx * kAttnRow);  // [G][D]
-  float* ps = qs + G * D;                                             // [L][G] probabilities
-  float* part = ps + kAttnMaxCtx * G;                                 // [8 slices][G][D]
-  __shared__ float red[32];
-  const int b = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
+  __shared__ __align__(16) uint16_t Ks[kAttnSplit * kAttnRow];
+  __shared__ __align__(16) uint16_t Vs[kAttnSplit * kAttnRow];
+  __shared__ __align__(16) float qs[G * D];
+  __shared__ float ps[G][kAttnSplit];
+  const int b = blockIdx.x, g = blockIdx.y, sp = blockIdx.z, tid = threadIdx.x;
   const int L = len[b];
+  const int t0 = sp * kAttnSplit;
+  if (t0 >= L) return;  // beyond this request's context: the merge ignores the split
+  const int n = min(kAttnSplit, L - t0);
   const size_t kv_stride = (size_t)n_kv * D;
-  const uint16_t* kb = kc + ((size_t)b * ctx_max * n_kv + g) * D;
-  const uint16_t* vb = vc + ((size_t)b * ctx_max * n_kv + g) * D;
-  // stage K, V (16 chunks of 16 B per row)
-  for (int i = tid; i < L * 16; i += kAttnThreads) {
+  const uint16_t* kb = kc + (((size_t)b * ctx_max + t0) * n_kv + g) * D;
+  const uint16_t* vb = vc + (((size_t)b * ctx_max + t0) * n_kv + g) * D;
+  for (int i = tid; i < n * 16; i += kAttnThreads) {
     const int t = i >> 4, c = i & 15;
-    *reinterpret_cast<uint4*>(Ks + t * kAttnRow + c * 8) = *reinterpret_cast<const uint4*>(kb + t * kv_stride + c * 8);
-    *reinterpret_cast<uint4*>(Vs + t * kAttnRow + c * 8) = *reinterpret_cast<const uint4*>(vb + t * kv_stride + c * 8);
+    *reinterpret_cast<uint4*>(Ks + t * kAttnRow + c * 8) = __ldg(reinterpret_cast<const uint4*>(kb + t * kv_stride + c * 8));
+    *reinterpret_cast<uint4*>(Vs + t * kAttnRow + c * 8) = __ldg(reinterpret_cast<const uint4*>(vb + t * kv_stride + c * 8));
   }
   for (int i = tid; i < G * D; i += kAttnThreads)
     qs[i] = bf16_to_f32(q[(size_t)b * ld_q + (size_t)g * G * D + i]) * scale;
   __syncthreads();
-  // scores
-  float sc[G];
-  float mx[G];
-#pragma unroll
-  for (int h = 0; h < G; ++h) { sc[h] = -INFINITY; }
-  for (int t = tid; t < L; t += kAttnThreads) {
-    float acc[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) acc[h] = 0.f;
+  // scores: thread -> (head h, positions t, t + 32 ...) with 128 / G threads per head
+  constexpr int TPH = kAttnThreads / G;
+  {
+    const int h = tid / TPH, j = tid % TPH;
+    for (int t = j; t < n; t += TPH) {
+      float acc = 0.f;
 #pragma unroll 4
-    for (int c = 0; c < 16; ++c) {
-      const uint4 k4 = *reinterpret_cast<const uint4*>(Ks + t * kAttnRow + c * 8);
-      const uint32_t* kk = reinterpret_cast<const uint32_t*>(&k4);
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
+      for (int c = 0; c < 16; ++c) {
+        const uint4 k4 = *reinterpret_cast<const uint4*>(Ks + t * kAttnRow + c * 8);
+        const uint32_t* kk = reinterpret_cast<const uint32_t*>(&k4);
         const float4 qa = *reinterpret_cast<const float4*>(qs + h * D + c * 8);
         const float4 qb = *reinterpret_cast<const float4*>(qs + h * D + c * 8 + 4);
-        float a = acc[h];
-        a = fmaf(qa.x, bf16_lo(kk[0]), a); a = fmaf(qa.y, bf16_hi(kk[0]), a);
-        a = fmaf(qa.z, bf16_lo(kk[1]), a); a = fmaf(qa.w, bf16_hi(kk[1]), a);
-        a = fmaf(qb.x, bf16_lo(kk[2]), a); a = fmaf(qb.y, bf16_hi(kk[2]), a);
-        a = fmaf(qb.z, bf16_lo(kk[3]), a); a = fmaf(qb.w, bf16_hi(kk[3]), a);
-        acc[h] = a;
+        acc = fmaf(qa.x, bf16_lo(kk[0]), acc); acc = fmaf(qa.y, bf16_hi(kk[0]), acc);
+        acc = fmaf(qa.z, bf16_lo(kk[1]), acc); acc = fmaf(qa.w, bf16_hi(kk[1]), acc);
+        acc = fmaf(qb.x, bf16_lo(kk[2]), acc); acc = fmaf(qb.y, bf16_hi(kk[2]), acc);
+        acc = fmaf(qb.z, bf16_lo(kk[3]), acc); acc = fmaf(qb.w, bf16_hi(kk[3]), acc);
       }
+      ps[h][t] = acc;
     }
-#pragma unroll
-    for (int h = 0; h < G; ++h) { ps[t * G + h] = acc[h]; }
   }
   __syncthreads();
-  // softmax per head
-#pragma unroll
-  for (int h = 0; h < G; ++h) {
+  // per-head max / exp / sum: warp w handles heads w, w + 4, ...
+  const int warp = tid >> 5, lane = tid & 31;
+  float* outp = part + (((size_t)b * gridDim.y + g) * G) * (size_t)S * kAttnPart;
+  for (int h = warp; h < G; h += kAttnThreads / 32) {
     float m = -INFINITY;
-    for (int t = tid; t < L; t += kAttnThreads) m = fmaxf(m, ps[t * G + h]);
-    mx[h] = block_max(m, red);
-  }
-  float sum[G];
+    for (int t = lane; t < n; t += 32) m = fmaxf(m, ps[h][t]);
 #pragma unroll
-  for (int h = 0; h < G; ++h) sum[h] = 0.f;
-  for (int t = tid; t < L; t += kAttnThreads) {
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.f;
+    for (int t = lane; t < n; t += 32) {
+      const float e = __expf(ps[h][t] - m);
+      ps[h][t] = e;
+      l += e;
+    }
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const float e = __expf(ps[t * G + h] - mx[h]);
-      ps[t * G + h] = e;
-      sum[h] += e;
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) {
+      float* pp = outp + ((size_t)h * S + sp) * kAttnPart;
+      pp[0] = m;
+      pp[1] = l;
     }
   }
-#pragma unroll
-  for (int h = 0; h < G; ++h) sc[h] = 1.f / block_sum(sum[h], red);
   __syncthreads();
-  // P.V: thread = (dim group dg of 4 dims, slice sl of positions)
-  const int dg = tid & 31, sl = tid >> 5;  // 32 groups x 8 slices
-  float o[G][4];
+  // P.V: thread = output dim d, all G heads
+  {
+    const int d = tid;
+    float o[G];
 #pragma unroll
-  for (int h = 0; h < G; ++h)
+    for (int h = 0; h < G; ++h) o[h] = 0.f;
+    for (int t = 0; t < n; ++t) {
+      const float v = bf16_to_f32(Vs[t * kAttnRow + d]);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[h][j] = 0.f;
-  for (int t = sl; t < L; t += 8) {
-    const uint2 v2 = *reinterpret_cast<const uint2*>(Vs + t * kAttnRow + dg * 4);
-    const float v0 = bf16_lo(v2.x), v1 = bf16_hi(v2.x), v2f = bf16_lo(v2.y), v3 = bf16_hi(v2.y);
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const float p = ps[t * G + h];
-      o[h][0] = fmaf(p, v0, o[h][0]); o[h][1] = fmaf(p, v1, o[h][1]);
-      o[h][2] = fmaf(p, v2f, o[h][2]); o[h][3] = fmaf(p, v3, o[h][3]);
+      for (int h = 0; h < G; ++h) o[h] = fmaf(ps[h][t], v, o[h]);
     }
-  }
 #pragma unroll
-  for (int h = 0; h < G; ++h)
-    *reinterpret_cast<float4*>(part + ((size_t)sl * G + h) * D + dg * 4) = make_float4(o[h][0], o[h][1], o[h][2], o[h][3]);
-  __syncthreads();
-  for (int i = tid; i < G * D; i += kAttnThreads) {
-    const int h = i / D, d = i % D;
-    float acc = 0.f;
-#pragma unroll
-    for (int s2 = 0; s2 < 8; ++s2) acc += part[((size_t)s2 * G + h) * D + d];
-    out[out_index(b, (g * G + h) * D + d, ld_out, out_np)] = __bfloat16_as_ushort(__float2bfloat16_rn(acc * sc[h]));
+    for (int h = 0; h < G; ++h) outp[((size_t)h * S + sp) * kAttnPart + 2 + d] = o[h];
   }
+}
+
+// Merge the splits of one (request, head): out = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s.
+__global__ void __launch_bounds__(128) attn_merge_kernel(const float* __restrict__ part, const int32_t* __restrict__ len,
+                                                         int n_heads, int S, uint16_t* __restrict__ out, int ld_out,
+                                                         int out_np) {
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  const int Sb = (len[b] + kAttnSplit - 1) / kAttnSplit;
+  const float* pp = part + ((size_t)b * n_heads + h) * (size_t)S * kAttnPart;
+  float M = -INFINITY;
+  for (int s2 = 0; s2 < Sb; ++s2) M = fmaxf(M, pp[(size_t)s2 * kAttnPart]);
+  float num = 0.f, den = 0.f;
+  for (int s2 = 0; s2 < Sb; ++s2) {
+    const float w = __expf(pp[(size_t)s2 * kAttnPart] - M);
+    den = fmaf(w, pp[(size_t)s2 * kAttnPart + 1], den);
+    num = fmaf(w, pp[(size_t)s2 * kAttnPart + 2 + d], num);
+  }
+  out[out_index(b, h * 128 + d, ld_out, out_np)] = __bfloat16_as_ushort(__float2bfloat16_rn(num / den));
 }
 
 // out = silu(gate) * up, gate/up halves of a [B][2I] row.
@@ -409,41 +412,38 @@ extern "C" int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_po
   return mesw_check_launch("rope_append");
 }
 
+extern "C" uint64_t mesw_attention_workspace_bytes(int B, int n_heads, int ctx_max) {
+  const int S = (ctx_max + kAttnSplit - 1) / kAttnSplit;
+  return (uint64_t)B * n_heads * S * kAttnPart * sizeof(float);
+}
+
 extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
                                      const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
                                      int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
-                                     int out_np, void* stream) {
-  if (B <= 0 || n_kv <= 0 || n_heads % n_kv) return mesw_fail(MESW_ERR_VALUE, "attention: bad shape");
+                                     int out_np, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (B <= 0 || n_kv <= 0 || n_heads % n_kv || ctx_max <= 0) return mesw_fail(MESW_ERR_VALUE, "attention: bad shape");
   if (head_dim != 128) return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: head_dim must be 128");
-  if (ctx_max > kAttnMaxCtx) return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: context window > 320");
+  if (!d_workspace || workspace_bytes < mesw_attention_workspace_bytes(B, n_heads, ctx_max))
+    return mesw_fail(MESW_ERR_VALUE, "attention: workspace too small (mesw_attention_workspace_bytes)");
   const int G = n_heads / n_kv;
-  const size_t smem = (size_t)2 * kAttnMaxCtx * kAttnRow * 2 +
-                      ((size_t)G * 128 + (size_t)kAttnMaxCtx * G + (size_t)8 * G * 128) * sizeof(float);
+  const int S = (ctx_max + kAttnSplit - 1) / kAttnSplit;
   const float scale = 1.0f / sqrtf((float)head_dim);
-  dim3 grid(B, n_kv);
+  dim3 grid(B, n_kv, S);
   cudaStream_t s = (cudaStream_t)stream;
-#define MESW_ATTN(GG)                                                                                   \
-  case GG: {                                                                                            \
-    static bool cfg = false;                                                                            \
-    if (!cfg) {                                                                                         \
-      cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<GG>,                                      \
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-      if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));                     \
-      cfg = true;                                                                                       \
-    }                                                                                                   \
-    mesw_launch(attn_decode_kernel<GG>, dim3(grid), dim3(kAttnThreads), smem, s, d_q, ld_q, d_kcache,         \
-                d_vcache, d_len, n_kv, ctx_max, scale, d_out, ld_out, out_np);                             \
-    break;                                                                                              \
-  }
+  float* part = reinterpret_cast<float*>(d_workspace);
+  cudaError_t e;
   switch (G) {
-    MESW_ATTN(1)
-    MESW_ATTN(2)
-    MESW_ATTN(4)
-    MESW_ATTN(8)
+    case 1: e = mesw_launch(attn_partial_kernel<1>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
+    case 2: e = mesw_launch(attn_partial_kernel<2>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
+    case 4: e = mesw_launch(attn_partial_kernel<4>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
+    case 8: e = mesw_launch(attn_partial_kernel<8>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
     default:
       return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: heads per kv head must be 1, 2, 4 or 8");
   }
-#undef MESW_ATTN
+  if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
+  e = mesw_launch(attn_merge_kernel, dim3(B, n_heads), dim3(128), 0, s, (const float*)part, d_len, n_heads, S, d_out,
+                  ld_out, out_np);
+  if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("attention_decode");
 }
 

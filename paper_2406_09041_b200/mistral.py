@@ -81,6 +81,8 @@ class MistralMultiExpert:
         self.logits = torch.zeros((B, self.g_head.n_pad), dtype=bf, device=dev)
         kv_shape = (self.n_layers, B, self.ctx_max, s.n_kv_heads, s.head_dim)
         self.kcache = torch.zeros(kv_shape, dtype=bf, device=dev)
+        self.attn_ws = torch.empty(int(_lib.lib().mesw_attention_workspace_bytes(B, s.n_heads, self.ctx_max)),
+                                   dtype=torch.uint8, device=dev)
         self.vcache = torch.zeros(kv_shape, dtype=bf, device=dev)
 
     def load_base(self, embedding, final_norm, head_w, layers: list) -> None:
@@ -265,7 +267,8 @@ class MistralMultiExpert:
                                    vc.data_ptr(), self.ctx_max, st))
             chk(L.mesw_attention_decode(self.qkv.data_ptr(), self.qkv.stride(0), kc.data_ptr(), vc.data_ptr(),
                                         self.len.data_ptr(), B, s.n_heads, s.n_kv_heads, s.head_dim,
-                                        self.ctx_max, self.attn.data_ptr(), 0, NP, st))
+                                        self.ctx_max, self.attn.data_ptr(), 0, NP, self.attn_ws.data_ptr(),
+                                        self.attn_ws.numel(), st))
             p_o(stream)
             chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), lw.mlp_norm.data_ptr(), B, H,
                                C.c_float(s.rms_eps), self.xn.data_ptr(), 0, NP, st))
