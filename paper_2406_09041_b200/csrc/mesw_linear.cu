@@ -45,7 +45,7 @@ constexpr int kMaxRows = 192;  // padded token rows per launch (TMEM: 2 * rows <
 constexpr int kMaxStages = 8;
 constexpr int kMaxCStages = 16;
 constexpr int kXRowGroupBytes = 2048;  // 8 token rows x 16 k-chunks x 16 B
-constexpr int kSalFast = 16;           // salient rows per column group handled from smem
+constexpr int kSalFast = 8;            // salient rows per column group handled from smem
 
 // Element index of x[t][k] in the canonical activation layout (see mesw.h): per 128-wide
 // k-step, two halves h = (t/8)%2 (rows 0-7 / 8-15 of every 16-row window), each a
@@ -509,63 +509,27 @@ __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S
 __device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& S, int cg, int cgp, int rank, int m,
                                           int t0, int p_first, int p_last, bool fast, const EpiPre& pre,
                                           const float* stage) {
-  const int NP = p.NP, HP = NP / 2;
+  const int NP = p.NP;
   const long long T2 = p.T, G2 = p.G / 2;
-  const int sg = S.tok2seg[t0];
-  int cb0 = t0 / 2, cb1 = HP + t0 / 2, cd0 = -1, cd1 = -1;
-  if (sg >= 0) {
-    const SegDesc& sd = S.segs[sg];
-    const int dw = (t0 - sd.win0) / 2;
-    cd0 = NP + sd.win0 + dw;
-    cd1 = NP + sd.win0 + sd.winN / 2 + dw;
-  }
-  const size_t slot_floats = (size_t)2 * NP * kUnitN;
+  const size_t slot_floats = (size_t)NP * kUnitN;
   float vb[16], vd[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) vb[i] = vd[i] = 0.f;
+  for (int i = 0; i < 16; ++i) vb[i] = vd[i] = 0.f;  // partials already hold base + s_j * delta
   for (int pp = p_first; pp <= p_last; ++pp) {
-    float lb[16], ld[16];
+    float lb[16];
     if (stage) {
-      const float* src = stage + (size_t)(pp - p_first) * slot_floats + m;
+      const float* src = stage + (size_t)(pp - p_first) * slot_floats + (size_t)t0 * kUnitN + m;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        lb[i] = src[(size_t)(cb0 + i) * kUnitN];
-        lb[8 + i] = src[(size_t)(cb1 + i) * kUnitN];
-      }
-      if (cd0 >= 0) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          ld[i] = src[(size_t)(cd0 + i) * kUnitN];
-          ld[8 + i] = src[(size_t)(cd1 + i) * kUnitN];
-        }
-      }
+      for (int i = 0; i < 16; ++i) lb[i] = src[(size_t)i * kUnitN];
     } else {
       const long long pu0 = (long long)pp * T2 / G2;
       const int s2 = 2 * (2 * pp + rank) + ((int)(pu0 / p.n_ks) == cgp ? 0 : 1);
-      const float* src = p.ws + (size_t)s2 * slot_floats + m;
+      const float* src = p.ws + (size_t)s2 * slot_floats + (size_t)t0 * kUnitN + m;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        lb[i] = __ldcg(src + (size_t)(cb0 + i) * kUnitN);
-        lb[8 + i] = __ldcg(src + (size_t)(cb1 + i) * kUnitN);
-      }
-      if (cd0 >= 0) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          ld[i] = __ldcg(src + (size_t)(cd0 + i) * kUnitN);
-          ld[8 + i] = __ldcg(src + (size_t)(cd1 + i) * kUnitN);
-        }
-      }
-    }
-    if (cd0 >= 0) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) vd[i] += ld[i];
+      for (int i = 0; i < 16; ++i) lb[i] = __ldcg(src + (size_t)i * kUnitN);
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) vb[i] += lb[i];
-  }
-  if (p.w == nullptr) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) vb[i] = 0.f;
   }
   epi_store16(p, S, cg, m, t0, vb, vd, fast, pre);
 }
@@ -972,19 +936,33 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
         }
       } else {
+        // stream-K partial: base + s_j * delta per row (natural row order, [NP][128] f32);
+        // the salient term, residual and activation are applied once, by the final reducer
         const int slot = 2 * c + (cgp == cgp_first ? 0 : 1);
-        const size_t slot_floats = (size_t)2 * NP * kUnitN;
+        const size_t slot_floats = (size_t)NP * kUnitN;
         float* mine = p.ws + (size_t)slot * slot_floats;
-        for (int t0 = 0; t0 < 2 * NP; t0 += 16) {
-          float v[16];
-          if (t0 < NP && !has_w) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        for (int t0 = 0; t0 < NP; t0 += 16) {
+          float vb[16], vd[16];
+          if (has_w) {
+            tmem_ld8(acc + (uint32_t)(t0 / 2), vb);
+            tmem_ld8(acc + (uint32_t)(HP + t0 / 2), vb + 8);
           } else {
-            tmem_ld16(acc + (uint32_t)t0, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vb[i] = 0.f;
+          }
+          const int sg = S.tok2seg[t0];
+          if (sg >= 0) {
+            const SegDesc& sd = S.segs[sg];
+            const int dw = (t0 - sd.win0) / 2;
+            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + dw), vd);
+            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + sd.winN / 2 + dw), vd + 8);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (pre.sg >= 0 && S.tok2seg[t0 + i] == pre.sg) vb[i] = fmaf(pre.sj, vd[i], vb[i]);
           }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) __stcg(mine + (size_t)(t0 + i) * kUnitN + mrow, v[i]);
+          for (int i = 0; i < 16; ++i) __stcg(mine + (size_t)(t0 + i) * kUnitN + mrow, vb[i]);
+          if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
         }
       }
       // accumulators consumed -> the leader may reuse this buffer
@@ -1041,32 +1019,56 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     const int fcg = S.fin.cg, fcgp = S.fin.cgp, pf = S.fin.p_first, pl = S.fin.p_last;
     const bool ffast = S.fin.fast != 0;
     const int fm = threadIdx.x % kUnitN;
-    // every contributor's whole slot in one bulk copy each, into the (now idle) smem ring
-    const size_t slot_bytes = (size_t)2 * NP * kUnitN * sizeof(float);
-    const bool staged = (size_t)(pl - pf + 1) * slot_bytes <= (size_t)p.ring_bytes;
-    if (staged && threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy partials -> TMA reads
-      mbar_arrive_expect_tx(&S.finbar, (uint32_t)((pl - pf + 1) * slot_bytes));
+    // Contributor slots are bulk-copied into the (now idle) smem ring in batches and summed,
+    // in contributor order, into region 0 -- one L2 round trip per batch however many pairs
+    // share the column group (small linears split a column group over many pairs).
+    const size_t slot_floats = (size_t)NP * kUnitN, slot_bytes = slot_floats * sizeof(float);
+    const int nC = pl - pf + 1;
+    const int nbuf = (int)((size_t)p.ring_bytes / slot_bytes);
+    const bool staged = nbuf >= 2 || nC == 1;
+    float* st = reinterpret_cast<float*>(ring);
+    const int t_first = 16 * (threadIdx.x / kUnitN);
+    EpiPre pre0;
+    if (t_first < NP) epi_prefetch(p, S, fcg, fm, t_first, ffast, pre0);  // in flight with the copies
+    MESW_PROF(long long fp[4] = {0, 0, 0, 0}; long long fq = clock64();)
+    if (staged) {
       const long long T2 = p.T, G2 = p.G / 2;
-      for (int pp = pf; pp <= pl; ++pp) {
-        const long long pu0 = (long long)pp * T2 / G2;
-        const int s2 = 2 * (2 * pp + (int)rank) + ((int)(pu0 / p.n_ks) == fcgp ? 0 : 1);
-        bulk_g2s(ring + (size_t)(pp - pf) * slot_bytes, p.ws + (size_t)s2 * (slot_bytes / sizeof(float)),
-                 (uint32_t)slot_bytes, &S.finbar);
+      uint32_t ph = 0;
+      for (int done = 0; done < nC;) {
+        const int region0 = done == 0 ? 0 : 1;
+        const int cnt = min(nC - done, nbuf - region0);
+        if (threadIdx.x == 0) {
+          // generic-proxy partials (global) and the smem the previous batch was read from ->
+          // async-proxy (bulk copy) accesses
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&S.finbar, (uint32_t)(cnt * slot_bytes));
+          for (int i = 0; i < cnt; ++i) {
+            const int pp = pf + done + i;
+            const long long pu0 = (long long)pp * T2 / G2;
+            const int s2 = 2 * (2 * pp + (int)rank) + ((int)(pu0 / p.n_ks) == fcgp ? 0 : 1);
+            bulk_g2s(ring + (size_t)(region0 + i) * slot_bytes, p.ws + (size_t)s2 * slot_floats, (uint32_t)slot_bytes,
+                     &S.finbar);
+          }
+        }
+        mbar_wait(&S.finbar, ph);
+        ph ^= 1;
+        for (int i = 1; i < region0 + cnt; ++i)
+          for (size_t e = threadIdx.x; e < slot_floats; e += kThreads) st[e] += st[(size_t)i * slot_floats + e];
+        __syncthreads();
+        done += cnt;
       }
     }
-    MESW_PROF(long long fp[4] = {0, 0, 0, 0}; long long fq = clock64();)
-    for (int t0 = 16 * (threadIdx.x / kUnitN); t0 < NP; t0 += 16 * (kThreads / kUnitN)) {
+    MESW_PROF(fp[1] += clock64() - fq; fq = clock64();)
+    for (int t0 = t_first; t0 < NP; t0 += 16 * (kThreads / kUnitN)) {
       EpiPre pre;
-      epi_prefetch(p, S, fcg, fm, t0, ffast, pre);  // in flight with the bulk copies
-      MESW_PROF(fp[0] += clock64() - fq; fq = clock64();)
-      if (staged) mbar_wait(&S.finbar, 0);
-      MESW_PROF(fp[1] += clock64() - fq; fq = clock64();)
-      reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre,
-                   staged ? reinterpret_cast<const float*>(ring) : nullptr);
+      if (t0 == t_first) pre = pre0;
+      else epi_prefetch(p, S, fcg, fm, t0, ffast, pre);
+      if (staged) reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pf, ffast, pre, st);
+      else reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre, nullptr);
       MESW_PROF(fp[2] += clock64() - fq; fq = clock64();)
     }
-    MESW_PROF(fp[3] = staged ? (pl - pf + 1) : -1;)
+    MESW_PROF(fp[3] = staged ? nC : -nC;)
     MESW_PROF(if (p.tbuf && threadIdx.x == 0) for (int i = 0; i < 4; ++i) p.tbuf[4096 * 40 + (size_t)blockIdx.x * 16 + i] = fp[i];)
     if (threadIdx.x == 0) p.counters[S.fin.cg] = 0;
     if (threadIdx.x == 0) MESW_STAMP(4);
