@@ -154,16 +154,31 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
     def step(i):
         plans[i % replicas]()
 
+    # the timed region replays one CUDA graph holding all K launches (no host launch gaps)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        graph.capture_begin()
+        for i in range(args.steps):
+            plans[i % replicas](cs)
+        graph.capture_end()
+    torch.cuda.current_stream().wait_stream(cs)
+
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph.replay()  # one untimed replay
+    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         st.record(stream)
-        for i in range(args.steps):
-            step(i)
+        graph.replay()
         en.record(stream)
         torch.cuda.synchronize()
     ms = st.elapsed_time(en)
