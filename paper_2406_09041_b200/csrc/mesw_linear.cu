@@ -766,6 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               MESW_PROF(tq = clock64();)
               mbar_wait_cluster(&S.afull[abase_own + aslot], aph);
               MESW_PROF(prof[3] += clock64() - tq;)
+              MESW_PROF(if (p.tbuf && blockIdx.x == 0 && lane == 0 && prof[7] < 32) p.tbuf[4096 * 56 + 512 + role * 64 + 2 * prof[7]] = clock64();)
               MESW_PROF(tq = clock64();)
               tc_fence_after();
               const int win0 = S.segs[q].win0;
@@ -782,6 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               tc2_commit_w(&S.aempty[abase_own + aslot]);
               if (++aslot == na_own) { aslot = 0; aph ^= 1; }
               MESW_PROF(prof[4] += clock64() - tq;)
+              MESW_PROF(if (p.tbuf && blockIdx.x == 0 && lane == 0 && prof[7] < 32) p.tbuf[4096 * 56 + 512 + role * 64 + 2 * prof[7] + 1] = clock64();)
               MESW_PROF(prof[7]++;)
             }
           }
@@ -851,8 +853,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
                 const int w0 = kh * WPK + 4 * v;
                 cw[w0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
               }
+            MESW_PROF(const bool jst = p.tbuf && blockIdx.x == 0 && threadIdx.x == kDqWarp0 * 32 + grp * 128 && dprof[7] < 32;)
+            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7]] = clock64();)
             MESW_PROF(dq = clock64();)
             if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
+            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 1] = clock64();)
             MESW_PROF(dprof[1] += clock64() - dq;)
             MESW_PROF(dq = clock64();)
             const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
@@ -868,6 +873,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               if (!(p.dbg & 4)) tmem_st32(a0 + lane_addr + 32 * kh, r);
             }
             MESW_PROF(dprof[2] += clock64() - dq;)
+            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 2] = clock64();)
             MESW_PROF(dq = clock64();)
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
@@ -877,6 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
             }
             MESW_PROF(dprof[3] += clock64() - dq;)
+            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 3] = clock64();)
             MESW_PROF(dprof[7]++;)
           }
           mbar_arrive(&S.cempty[sc]);  // every thread: release orders its own smem reads
@@ -908,7 +915,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       const bool fast = gather_salient_x(p, S, cg, gtid);
       EpiPre pre;
       epi_prefetch(p, S, cg, mrow, 0, fast, pre);
-      mbar_wait(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
+      if (p.dbg & 128) mbar_wait(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
+      else mbar_wait_sleep(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
       tc_fence_after();
       if (gtid == 0 && pi == po.np - 1) MESW_STAMP(5);
       const uint32_t acc = tbase + lane_addr + (uint32_t)(ab * 2 * NP);
@@ -1243,6 +1251,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
         const int cols = kTmemCols - n_acc * 2 * p.NP;
         int slots = cols / kAColsPerSlot;
         if (slots > kMaxASlots) slots = kMaxASlots;
+        if (getenv("MESW_MAXSLOTS") && slots > atoi(getenv("MESW_MAXSLOTS"))) slots = atoi(getenv("MESW_MAXSLOTS"));
         if (cols < 0 || slots < n_delta) continue;
         // every issuer with delta jobs gets >= 1 slot; the rest go to the most loaded
         int jobs[3] = {0, 0, 0};

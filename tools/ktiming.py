@@ -46,8 +46,9 @@ for g in range(2):
     for r, nm in ((0, "lead"), (1, "peer")):
         print(f"  deq{g} {nm}", " ".join(f"{pd[i]}={np.median(dprof[r::2, g, i]):.0f}" for i in range(8) if pd[i] != "-"))
 eprof = buf[4096 * 40:4096 * 40 + G * 16].reshape(G, 16).astype(np.int64)
-sel = eprof[:, 0] > 0
-print("  final red (cycles):", " ".join(f"{n}={np.median(eprof[sel, i]):.0f}/{np.max(eprof[sel, i]):.0f}" for i, n in enumerate(["prefetch_issue", "stage_wait", "reduce+store", "ncontrib"])), f"n={sel.sum()}")
+sel = eprof[:, 2] > 0
+if sel.any():
+  print("  final red (cycles):", " ".join(f"{n}={np.median(eprof[sel, i]):.0f}/{np.max(eprof[sel, i]):.0f}" for i, n in enumerate(["prefetch_issue", "stage_wait", "reduce+store", "ncontrib"])), f"n={sel.sum()}")
 tl = buf[4096 * 56:4096 * 56 + 260].astype(np.int64)
 t0c = tl[256]
 if t0c:
@@ -56,3 +57,16 @@ if t0c:
         v = v[v > 0]
         if v.size:
             print(f"  {nm:22s}", " ".join(f"{(x - t0c):6d}" for x in v[:30]))
+jb = buf[4096 * 56 + 512:4096 * 56 + 1024].astype(np.int64)
+if t0c:
+    for r in range(3):
+        v = jb[r * 64:r * 64 + 64].reshape(32, 2)
+        v = v[v[:, 0] > 0]
+        if v.size:
+            print(f"  issuer{r} jobs (afull-ready, committed):", " ".join(f"{a - t0c}/{b - a}" for a, b in v[:16]))
+    for g in range(2):
+        v = jb[256 + g * 128:256 + g * 128 + 128].reshape(32, 4)
+        v = v[v[:, 0] > 0]
+        if v.size:
+            print(f"  deq{g} jobs (start, +slot, +stored, +arrived):",
+                  " ".join(f"{a - t0c}/{b - a}/{c - b}/{d - c}" for a, b, c, d in v[:14]))
