@@ -37,6 +37,27 @@ class LayerWeights:
     down: DeviceWeight
 
 
+def _launch_groups(B: int, segs: list) -> list:
+    """Split engine rows [0, B) into launch groups of <= MAX_ROWS rows at 16-row boundaries
+    (segment boundaries preferred; an oversized expert group is cut too).  Returns
+    [(r0, r1, segments rebased to r0)]."""
+    from .device import MAX_ROWS
+    cuts = [0]
+    bounds = sorted({b for b, _, _ in segs} | {B})
+    for b in bounds:
+        while b - cuts[-1] > MAX_ROWS:
+            # last segment start inside the window, else a 16-row cut
+            inside = [x for x in bounds if cuts[-1] < x <= cuts[-1] + MAX_ROWS and x % 16 == 0 and x < b]
+            cuts.append(inside[-1] if inside else cuts[-1] + MAX_ROWS)
+    if cuts[-1] != B:
+        cuts.append(B)
+    groups = []
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        gs = [(max(b, r0) - r0, min(e, r1) - r0, sl) for b, e, sl in segs if b < r1 and e > r0]
+        groups.append((r0, r1, gs))
+    return groups
+
+
 class MistralMultiExpert:
     """Base model + resident experts + decode buffers for up to `max_batch` requests."""
 
@@ -72,12 +93,9 @@ class MistralMultiExpert:
         self.pos = torch.zeros(B, dtype=torch.int32, device=dev)
         self.len = torch.ones(B, dtype=torch.int32, device=dev)
         self.h = torch.zeros((B, s.hidden), dtype=bf, device=dev)
-        # inputs of the fused linears live in the canonical tile layout (include/mesw.h)
-        self.xn = torch.zeros(canonical_numel(B, s.hidden), dtype=bf, device=dev)
+        # (the fused linears' inputs live in per-launch-group canonical buffers: _build_plans)
         self.qkv = torch.zeros((B, self.g_qkv.n_pad), dtype=bf, device=dev)
-        self.attn = torch.zeros(canonical_numel(B, self.g_o.m), dtype=bf, device=dev)
         self.gu = torch.zeros((B, self.g_gu.n_pad), dtype=bf, device=dev)
-        self.act = torch.zeros(canonical_numel(B, self.g_down.m), dtype=bf, device=dev)
         self.logits = torch.zeros((B, self.g_head.n_pad), dtype=bf, device=dev)
         kv_shape = (self.n_layers, B, self.ctx_max, s.n_kv_heads, s.head_dim)
         self.kcache = torch.zeros(kv_shape, dtype=bf, device=dev)
@@ -208,9 +226,11 @@ class MistralMultiExpert:
         if (pl_req >= self.ctx_max).any():
             raise ValueError("prompt longer than the cache window")
         pl = np.where(rows >= 0, pl_req[np.maximum(rows, 0)], 0)
+        groups = _launch_groups(B, segs)
         if getattr(self, "B", None) != B or getattr(self, "segments", None) != segs:
             self._plans = None  # launch geometry changed: rebuild plans / re-capture
             self.graph = None
+        self.groups = groups
         self.B = B
         self.n_requests = n
         self.rows = rows
@@ -230,61 +250,85 @@ class MistralMultiExpert:
 
     # ------------------------------------------------------------------ step
     def _build_plans(self):
-        B, s, segs = self.B, self.shape, self.segments
-        plans = []
-        for l, lw in enumerate(self.layers):
-            tq, to, tgu, td = self.tables[l]
-            plans.append((
-                LinearPlan(self.xn, B, lw.qkv, tq if segs else None, segs, self.qkv[:B]),
-                LinearPlan(self.attn, B, lw.o, to if segs else None, segs, self.h[:B], residual=self.h[:B]),
-                LinearPlan(self.xn, B, lw.gateup, tgu if segs else None, segs, self.gu[:B]),
-                LinearPlan(self.act, B, lw.down, td if segs else None, segs, self.h[:B], residual=self.h[:B]),
-            ))
-        head = LinearPlan(self.xn, B, self.head, None, [], self.logits[:B])
-        self._plans = (plans, head)
+        """Per launch group (rows [r0, r1), <= MAX_ROWS padded rows, segments rebased): its
+        canonical input buffers and the fused-linear plans of every layer + lm_head."""
+        s = self.shape
+        gplans = []
+        for (r0, r1, segs) in self.groups:
+            rows = r1 - r0
+            bufs = {
+                "xn": torch.zeros(canonical_numel(rows, s.hidden), dtype=torch.bfloat16, device=self.device),
+                "attn": torch.zeros(canonical_numel(rows, self.g_o.m), dtype=torch.bfloat16, device=self.device),
+                "act": torch.zeros(canonical_numel(rows, self.g_down.m), dtype=torch.bfloat16, device=self.device),
+            }
+            h, qkv, gu = self.h[r0:r1], self.qkv[r0:r1], self.gu[r0:r1]
+            layers = []
+            for l, lw in enumerate(self.layers):
+                tq, to, tgu, td = self.tables[l]
+                layers.append((
+                    LinearPlan(bufs["xn"], rows, lw.qkv, tq if segs else None, segs, qkv),
+                    LinearPlan(bufs["attn"], rows, lw.o, to if segs else None, segs, h, residual=h),
+                    LinearPlan(bufs["xn"], rows, lw.gateup, tgu if segs else None, segs, gu),
+                    LinearPlan(bufs["act"], rows, lw.down, td if segs else None, segs, h, residual=h),
+                ))
+            head = LinearPlan(bufs["xn"], rows, self.head, None, [], self.logits[r0:r1])
+            gplans.append((r0, r1, bufs, layers, head))
+        self._plans = gplans
 
     def step(self, stream=None) -> None:
-        """One decode step for the whole batch: ids (engine order) -> next ids in self.ids."""
+        """One decode step for the whole batch: ids (engine order) -> next ids in self.ids.
+        Batches wider than one fused launch (> MAX_ROWS padded rows, e.g. many experts)
+        run as several launch groups; each re-streams the base weights."""
         if self._plans is None:
             self._build_plans()
         L = _lib.lib()
         st = _stream(stream)
         s, B = self.shape, self.B
         chk = _lib.check
-        plans, head = self._plans
         H = s.hidden
-        NP = canonical_rows(B)
+        eps = C.c_float(s.rms_eps)
+        bf = 2  # bytes per bf16
+
+        def rows_ptr(t, r0):
+            return t.data_ptr() + r0 * t.stride(0) * bf
+
         chk(L.mesw_embed(self.ids.data_ptr(), B, self.embedding.data_ptr(), H, self.h.data_ptr(),
                          self.h.stride(0), st))
         for l, lw in enumerate(self.layers):
-            p_qkv, p_o, p_gu, p_down = plans[l]
-            chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), lw.attn_norm.data_ptr(), B, H,
-                               C.c_float(s.rms_eps), self.xn.data_ptr(), 0, NP, st))
-            p_qkv(stream)
+            for (r0, r1, bufs, layers, _) in self._plans:
+                chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), lw.attn_norm.data_ptr(), r1 - r0, H, eps,
+                                   bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+                layers[l][0](stream)
             kc, vc = self.kcache[l], self.vcache[l]
             chk(L.mesw_rope_append(self.qkv.data_ptr(), self.qkv.stride(0), self.pos.data_ptr(), B, s.n_heads,
                                    s.n_kv_heads, s.head_dim, C.c_float(s.rope_theta), kc.data_ptr(),
                                    vc.data_ptr(), self.ctx_max, st))
-            chk(L.mesw_attention_decode(self.qkv.data_ptr(), self.qkv.stride(0), kc.data_ptr(), vc.data_ptr(),
-                                        self.len.data_ptr(), B, s.n_heads, s.n_kv_heads, s.head_dim,
-                                        self.ctx_max, self.attn.data_ptr(), 0, NP, self.attn_ws.data_ptr(),
-                                        self.attn_ws.numel(), st))
-            p_o(stream)
-            chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), lw.mlp_norm.data_ptr(), B, H,
-                               C.c_float(s.rms_eps), self.xn.data_ptr(), 0, NP, st))
-            p_gu(stream)
-            chk(L.mesw_swiglu(self.gu.data_ptr(), self.gu.stride(0), B, s.intermediate, self.act.data_ptr(),
-                              0, NP, st))
-            p_down(stream)
-        chk(L.mesw_rmsnorm(self.h.data_ptr(), self.h.stride(0), self.final_norm.data_ptr(), B, H,
-                           C.c_float(s.rms_eps), self.xn.data_ptr(), 0, NP, st))
-        head(stream)
+            for (r0, r1, bufs, layers, _) in self._plans:
+                chk(L.mesw_attention_decode(rows_ptr(self.qkv, r0), self.qkv.stride(0), rows_ptr(kc, r0),
+                                            rows_ptr(vc, r0), self.len.data_ptr() + 4 * r0, r1 - r0, s.n_heads,
+                                            s.n_kv_heads, s.head_dim, self.ctx_max, bufs["attn"].data_ptr(), 0,
+                                            canonical_rows(r1 - r0), self.attn_ws.data_ptr(), self.attn_ws.numel(),
+                                            st))
+                layers[l][1](stream)
+            for (r0, r1, bufs, layers, _) in self._plans:
+                chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), lw.mlp_norm.data_ptr(), r1 - r0, H, eps,
+                                   bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+                layers[l][2](stream)
+            for (r0, r1, bufs, layers, _) in self._plans:
+                chk(L.mesw_swiglu(rows_ptr(self.gu, r0), self.gu.stride(0), r1 - r0, s.intermediate,
+                                  bufs["act"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+                layers[l][3](stream)
+        for (r0, r1, bufs, _, head) in self._plans:
+            chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), self.final_norm.data_ptr(), r1 - r0, H, eps,
+                               bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+            head(stream)
         chk(L.mesw_argmax(self.logits.data_ptr(), 1, B, s.vocab, self.logits.stride(0), self.ids.data_ptr(), st))
         chk(L.mesw_advance_positions(self.pos.data_ptr(), self.len.data_ptr(), B, self.ctx_max,
                                      min(self.ctx_max - 1, 128), st))
 
     def launches_per_step(self) -> int:
-        return 1 + 9 * self.n_layers + 4
+        g = len(self.groups)
+        return 1 + (1 + g * 9) * self.n_layers + g * 2 + 2  # attention is 2 kernels
 
     def capture(self) -> None:
         """Capture one decode step in a CUDA graph (replayed by `replay`)."""

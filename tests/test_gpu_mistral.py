@@ -39,7 +39,7 @@ def _build(shape, n_experts=3, seed=0, B=5):
         lw["attn_norm"] = _bf(1 + 0.1 * rng.normal(size=s.hidden))
         lw["mlp_norm"] = _bf(1 + 0.1 * rng.normal(size=s.hidden))
         W["layers"].append(lw)
-    eng = MistralMultiExpert(s, max_batch=64, ctx_max=32)
+    eng = MistralMultiExpert(s, max_batch=256, ctx_max=32)
     eng.load_base(torch.from_numpy(W["embedding"]), torch.from_numpy(W["final_norm"]),
                   torch.from_numpy(W["head"]),
                   [{k: torch.from_numpy(v) for k, v in lw.items()} for lw in W["layers"]])
@@ -60,13 +60,19 @@ def _build(shape, n_experts=3, seed=0, B=5):
     return eng, W, dense
 
 
-def test_decode_step_matches_oracle():
+@pytest.mark.parametrize("n_exp,experts", [
+    (3, ["e1", "e0", "e2", "e1", None]),
+    # 13 expert windows of 16 rows = 208 rows > one launch: two launch groups per linear
+    (13, [f"e{i}" for i in range(13)] + ["e3", None]),
+])
+def test_decode_step_matches_oracle(n_exp, experts):
     import torch
     shape = _mini()
-    eng, W, dense = _build(shape)
-    B, prompt = 5, 6
-    experts = ["e1", "e0", "e2", "e1", None]
+    eng, W, dense = _build(shape, n_experts=n_exp)
+    B, prompt = len(experts), 6
     rows = eng.set_batch(experts, [prompt] * B)
+    if n_exp > 12:
+        assert len(eng.groups) == 2
     R = eng.B
     real = np.flatnonzero(rows >= 0)  # engine rows holding requests
     assert sorted(rows[real].tolist()) == list(range(B))
@@ -84,7 +90,7 @@ def test_decode_step_matches_oracle():
     torch.cuda.synchronize()
     logits = eng.logits[:R, :shape.vocab].float().cpu().numpy()[real]
     nxt = eng.ids[:R].cpu().numpy()[real]
-    slot = {f"e{i}": i for i in range(3)}
+    slot = {f"e{i}": i for i in range(n_exp)}
     exp_of = [slot[experts[rows[r]]] if experts[rows[r]] is not None else -1 for r in real]
     kco = [[kc[l][r].astype(np.float64).copy() for r in real] for l in range(shape.n_layers)]
     vco = [[vc[l][r].astype(np.float64).copy() for r in real] for l in range(shape.n_layers)]
