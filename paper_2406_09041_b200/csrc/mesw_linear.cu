@@ -115,7 +115,7 @@ struct Smem {
   SegDesc segs[MESW_MAX_SEGMENTS];
   int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
   int8_t seg_iss[MESW_MAX_SEGMENTS];                         // MMA issuer of each segment
-  float xsal[kMaxRows][16];  // x[t][salient idx r] of the current column group (k <= 16 fast path)
+  float xsal[kMaxRows][kSalFast];  // x[t][salient idx r] of the current column group (fast path)
 };
 
 __host__ __device__ inline size_t ring_offset() { return (sizeof(Smem) + 1023) & ~size_t(1023); }
@@ -1217,6 +1217,16 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
       p.nw = a->w ? D : 0;
       p.nc = D * p.n_chunks;
       break;
+    }
+    {  // code-heavy launches: two units of weights / activations, the code ring gets the rest
+      const size_t wx = 2 * ((a->w ? (size_t)kUnitWBytes : 0) + (size_t)p.xbytes) + 1024;
+      const int nc = budget > wx ? (int)std::min<size_t>(kMaxCStages, (budget - wx) / p.cbytes) : 0;
+      if (nc >= 2) {
+        p.nx = 2;
+        p.nw = a->w ? 2 : 0;
+        p.nc = nc;
+        break;
+      }
     }
     if (p.segs_per_chunk <= kDqGroups) return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory: fewer than 2 stages");
     p.segs_per_chunk = (p.segs_per_chunk / 2 + kDqGroups - 1) / kDqGroups * kDqGroups;  // smaller chunks
