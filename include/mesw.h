@@ -230,6 +230,19 @@ int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int ld, int32_t
 int mesw_advance_positions(int32_t* d_pos, int32_t* d_len, int B, int ctx_max, int wrap_to,
                            void* stream);
 
+/* ------------------------------------------------ f2: delta compression
+ * Replaces compress.compress_layer (compress.py:178-215, metric "reconstruction"),
+ * bit-exact: steps, salient indices, fp16 salient rows and packed codes equal the
+ * reference's for the same f32 delta [m][n] (reference orientation: rows = input
+ * channels) and f32 activation energies [m] (ActivationStats.energy).  Outputs:
+ * d_steps f32[n], d_sal_idx int32[k] ascending, d_sal_rows binary16[k][n],
+ * d_packed mesw_packed_nbytes(m, n, bits) bytes (column-major runs, LSB-first).  */
+uint64_t mesw_compress_workspace_bytes(uint32_t m, uint32_t n);
+int mesw_compress_layer(const float* d_delta, uint32_t m, uint32_t n, const float* d_energy,
+                        uint32_t bits, uint32_t k, float* d_steps, int32_t* d_sal_idx,
+                        uint16_t* d_sal_rows, uint8_t* d_packed, void* d_workspace,
+                        uint64_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------ K4: model-level router
  * Replaces SPEC router.classify for a batch of B queries:
  * multinomial Naive Bayes over FNV-1a-hashed character 2/3-grams (2^16 buckets),

@@ -34,6 +34,7 @@ __all__ = [
     "save_artifact",
     "layer_block_nbytes",
     "compressed_size_bytes",
+    "compress_layer",
 ]
 
 MAGIC = b"MESW"
@@ -201,3 +202,46 @@ def compressed_size_bytes(artifact: ExpertArtifact) -> SizeBreakdown:
     fh = len(MAGIC) + 2 + 4 + len(artifact.manifest.to_json())
     return SizeBreakdown(file_header=fh, layers=[
         layer_block_nbytes(l.rows, l.cols, l.bits, l.salient.k) for l in artifact.layers])
+
+
+def compress_layer(delta, stats, bits: int = 2, salient_k: int = 8, metric: str = "reconstruction",
+                   device="cuda") -> CompressedDelta:
+    """compress.compress_layer (compress.py:178-215) on the GPU, bit-exact with the
+    reference for metric "reconstruction" (mesw_compress_layer, csrc/mesw_compress.cu).
+
+    delta: f32 [m, n] (reference orientation: rows = input channels), numpy or torch;
+    stats: ActivationStats-like (`.energy` f32 [m]) or the energy vector itself."""
+    import torch
+    if metric != "reconstruction":
+        raise NotImplementedError("the GPU compressor implements the default 'reconstruction' metric")
+    energy = getattr(stats, "energy", stats)
+    if energy is None:
+        raise ValueError("metric 'reconstruction' requires activation stats")
+    dev = torch.device(device)
+    d = torch.as_tensor(np.asarray(delta, np.float32) if not torch.is_tensor(delta) else delta).to(
+        dev, torch.float32).contiguous()
+    if d.ndim != 2:
+        raise ValueError(f"expected a 2-D delta, got shape {tuple(d.shape)}")
+    m, n = d.shape
+    if salient_k > m:
+        raise ValueError(f"salient_k={salient_k} exceeds {m} input channels")
+    e = torch.as_tensor(np.asarray(energy, np.float32)).to(dev).contiguous()
+    if e.shape != (m,):
+        raise ValueError(f"stats cover {e.shape[0]} channels, delta has {m} rows")
+    L = _lib.lib()
+    steps = torch.empty(n, dtype=torch.float32, device=dev)
+    idx = torch.empty(max(salient_k, 1), dtype=torch.int32, device=dev)
+    rows = torch.empty((max(salient_k, 1), n), dtype=torch.int16, device=dev)
+    packed = torch.empty(int(L.mesw_packed_nbytes(m, n, bits)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(L.mesw_compress_workspace_bytes(m, n)), dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream(dev)
+    _lib.check(L.mesw_compress_layer(d.data_ptr(), m, n, e.data_ptr(), bits, salient_k, steps.data_ptr(),
+                                     idx.data_ptr(), rows.data_ptr(), packed.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     C.c_void_p(s.cuda_stream)))
+    s.synchronize()
+    k = salient_k
+    return CompressedDelta(
+        salient=SalientSet(indices=idx[:k].cpu().numpy().astype(np.int64), k=k),
+        salient_rows=rows[:k].cpu().numpy().view(np.float16).reshape(k, n),
+        steps=steps.cpu().numpy(),
+        packed=PackedCodes(bits=bits, rows=m, cols=n, data=packed.cpu().numpy().tobytes()))

@@ -149,6 +149,8 @@ def layer_fixtures(rng, kat_out):
         arrays[f"{name}_recon"] = layer.reconstruct()
         arrays[f"{name}_codes"] = layer.codes()
         arrays[f"{name}_salient"] = layer.salient.indices
+        arrays[f"{name}_delta"] = delta            # compress_layer inputs (GPU compression parity)
+        arrays[f"{name}_energy"] = stats.energy
         names.append(name)
     np.savez_compressed(os.path.join(HERE, "layer_expected.npz"), **arrays)
     kat_out["layers"] = names

@@ -71,6 +71,7 @@ if __name__ == "__main__":
     ap.add_argument("--experts", type=int, default=3)
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--ctas", type=int, default=0)
     a = ap.parse_args()
     if a.sweep:
         for (m, n) in [(4096, 14336), (4096, 6144), (4096, 4096), (14336, 4096), (4096, 28672)]:
@@ -81,4 +82,4 @@ if __name__ == "__main__":
         run(4096, 14336, 16, 32, a.reps)
         run(4096, 14336, 3, 8, a.reps, base=False)
     else:
-        run(a.m, a.n, a.experts, a.batch, a.reps)
+        run(a.m, a.n, a.experts, a.batch, a.reps, num_ctas=a.ctas)
