@@ -7,6 +7,7 @@ Workloads (BASELINE.json configs):
       deltas on all 224 decoder linears, mixed-expert batch decode (one step = one token
       for every request in the batch).
   c1: one 4096x14336 MLP linear, 3 experts, batch-8 mixed decode (the CPU-runnable case).
+  c4: prefill of 2048 tokens over 16 experts through the same linear (tensor-bound roofline).
 
 Under torchrun (N>1) every rank serves its own expert shard (experts placed e mod G,
 replicated base, no collective on the data path): weak scaling, value = all tokens / max time.
@@ -97,7 +98,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--experts", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

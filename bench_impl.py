@@ -100,6 +100,19 @@ def reference_arm(args):
                 "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
                                  "sample": "full C1 step: x@W + x_g@reconstruct() per expert group (numpy)"},
                 "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if args.config == "c4":
+        for _ in range(min(args.warmup, 1)):
+            _c4_cpu()
+        dts = [_c4_cpu() for _ in range(args.steps)]
+        val = C4_T / (sum(dts) / len(dts))
+        return {"impl": "reference", "metric": "prefill tokens/sec, one Mistral MLP linear 4096x14336, 2048 tokens over 16 experts",
+                "value": val, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * C4_T / val, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "c4: prefill 2048 tokens x 16 experts (128 each), 4096x14336 fused linear"},
+                "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
+                                 "sample": "per step: 1 expert group of 128 tokens (x_g@W + x_g@reconstruct), x16"},
+                "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     from bench_mistral import reference_arm_c2
     return reference_arm_c2(args)
 
@@ -234,7 +247,106 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
     return line
 
 
+C4_T, C4_E = 2048, 16
+
+
+def _c4_cpu(max_groups: int = 1):
+    """Reference algorithm for one expert group of the prefill (x_g@W + x_g@reconstruct),
+    timed and scaled to all groups (bounded sample)."""
+    from paper_2406_09041_b200 import compress, synth
+    rng = np.random.default_rng(0)
+    W = rng.normal(0, 0.02, size=(C1_M, C1_N)).astype(np.float32)
+    art = compress.deserialize_artifact(synth.synthetic_expert_artifact(1, [(C1_M, C1_N)], "e0"))
+    layer = _oracle_layers([art])[0]
+    x = rng.normal(0, 1, size=(C4_T // C4_E, C1_M)).astype(np.float32)
+    t0 = time.perf_counter()
+    for _ in range(max_groups):
+        _ = x @ W + x @ layer.reconstruct()
+    return (time.perf_counter() - t0) / max_groups * C4_E
+
+
+def run_c4(args, ws, rank, local, ClockSampler, peaks):
+    """C4: prefill of 2048 tokens (16 experts x 128) through one 4096x14336 fused linear:
+    base GEMM and delta contraction on tcgen05 (one launch per expert group of 128 rows)."""
+    import json
+    import torch
+    from paper_2406_09041_b200 import compress, synth
+    from paper_2406_09041_b200.device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan,
+                                               pack_x)
+    geom = LinearGeometry(C1_M, (C1_N,))
+    g = torch.Generator(device="cuda").manual_seed(rank)
+    dw = DeviceWeight.empty(geom)
+    dw.load_block(0, (torch.randn((C1_M, C1_N), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+    table = ExpertTable("cuda")
+    for e in range(C4_E):
+        blob = synth.synthetic_expert_artifact(100 + e, [(C1_M, C1_N)], f"e{e}")
+        table.set(e, DeviceDelta.from_blocks([compress.deserialize_artifact(blob).layers[0]], geom))
+    per = C4_T // C4_E
+    x = torch.randn((C4_T, C1_M), generator=g, device="cuda").to(torch.bfloat16)
+    y = torch.empty((C4_T, C1_N), dtype=torch.bfloat16, device="cuda")
+    plans = [LinearPlan(pack_x(x[e * per:(e + 1) * per].contiguous()), per, dw, table, [(0, per, e)],
+                        y[e * per:(e + 1) * per], geom=geom) for e in range(C4_E)]
+    for _ in range(args.warmup):
+        for p in plans:
+            p()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    stream = torch.cuda.current_stream()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        st.record(stream)
+        for _ in range(args.steps):
+            for p in plans:
+                p()
+        en.record(stream)
+        torch.cuda.synchronize()
+    ms_t = torch.tensor([st.elapsed_time(en) / args.steps], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    flops = 2.0 * C4_T * C1_M * C1_N * 2  # base + delta contraction
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+        pk = json.load(f)
+    peak = float(pk.get("bf16_tflops", 1590.0))
+    achieved = flops / (ms / 1e3) / 1e12
+    # e2e: host x (pinned) -> device, pack + fused launches, y -> host
+    xh = x.cpu().pin_memory()
+    yh = torch.empty((C4_T, C1_N), dtype=torch.bfloat16).pin_memory()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x.copy_(xh, non_blocking=True)
+        for e, p in enumerate(plans):
+            pack_x(x[e * per:(e + 1) * per].contiguous(), out=p.keep[0])  # canonical layout of the fresh input
+            p()
+        yh.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    line = {
+        "metric": "prefill tokens/sec, one Mistral MLP linear 4096x14336, 2048 tokens over 16 experts",
+        "value": ws * C4_T / (ms / 1e3), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "c4: prefill 2048 tokens x 16 experts (128 each), 4096x14336 fused linear",
+                   "launches_per_step": C4_E},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": "measured burst",
+                     "flops_per_step": flops, "kernel": "me_linear_tc_kernel<2>"},
+        "e2e": {"value": ws * C4_T / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(xh.numel() * 2),
+                "d2h_bytes_per_step": int(yh.numel() * 2)},
+        "gpu_launches": C4_E * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        dt = _c4_cpu()
+        line["cpu_baseline"] = {"value": C4_T / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": "1 expert group of 128 tokens (x_g@W + x_g@reconstruct) timed, x16"}
+    return line
+
+
 def run_ours(args, ws, rank, local, ClockSampler, peaks):
+    if args.config == "c4":
+        return run_c4(args, ws, rank, local, ClockSampler, peaks)
     if args.config == "c1":
         return run_c1(args, ws, rank, local, ClockSampler, peaks)
     from bench_mistral import run_c2
