@@ -23,6 +23,7 @@ from .compress import CompressedDelta
 from .device import DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, me_linear
 
 __all__ = [
+    "base_digest",
     "GpuCompressedProvider",
     "ExactProvider",
     "LowRankProvider",
@@ -37,6 +38,20 @@ __all__ = [
 
 _MAX_ROWS = 32  # hi/lo token pairs per launch (kernel handles <= 64 tokens)
 
+
+def base_digest(model) -> str:
+    """toylm.base_digest (toylm.py:115-120): SHA-256 over the little-endian f32 bytes of the
+    base matrices in `weight_matrices()` order (embedding, hidden layers..., head) -- the
+    identity an expert artifact's manifest binds to.  Host-side, computed once at load.
+    `model`: anything with weight_matrices(), or an iterable of matrices."""
+    import hashlib
+    mats = model.weight_matrices() if hasattr(model, "weight_matrices") else model
+    h = hashlib.sha256()
+    for w in mats:
+        if hasattr(w, "detach"):
+            w = w.detach().float().cpu().numpy()
+        h.update(np.ascontiguousarray(w, dtype="<f4").tobytes())
+    return h.hexdigest()
 
 def split_bf16(x: torch.Tensor, m_pad: int) -> torch.Tensor:
     """f32 [T, m] -> bf16 [2T, m_pad]: rows 0..T-1 = bf16(x), rows T.. = bf16(x - hi)."""

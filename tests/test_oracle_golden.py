@@ -104,3 +104,14 @@ def test_toy_forward_with_delta_matches_reference():
         np.testing.assert_allclose(ot.forward_with_delta(base, provs, toks), ze[f"fwd_delta_{e}"],
                                    rtol=1e-5, atol=1e-5)
         assert ot.greedy_decode(base, ze["prompt"], 12, provs) == ze[f"greedy_{e}"].tolist()
+
+
+def test_base_digest_matches_reference_manifests():
+    """toylm.base_digest (toylm.py:115-120): the toy experts were compressed against toy_base."""
+    from oracle import mesw as om
+    from paper_2406_09041_b200.infer import base_digest
+    z = np.load(os.path.join(GOLDEN, "toy_base.npz"))
+    mats = [z["embedding"]] + [z[f"layer{i}"] for i in range(4)] + [z["head"]]
+    with open(os.path.join(GOLDEN, "toy_expert_0.mesw"), "rb") as f:
+        man, _ = om.parse_artifact(f.read())
+    assert base_digest(mats) == man["base_digest"]
