@@ -98,7 +98,7 @@ struct LinearParams {
   int ring_bytes;  // dynamic shared memory past the Smem header
   int n_iss;  // MMA issuer threads (a tcgen05.mma stream runs ~60-85 cycles/instr per issuer)
   unsigned long long* tbuf;  // MESW_TIMING: per-CTA globaltimer stamps
-  int dbg;  // perf experiments: bit0 skip dequant math, bit1 skip delta MMAs, bit2 skip tcgen05.st
+  int dbg;  // reserved (MESW_DBG)
 };
 
 struct Smem {
@@ -633,14 +633,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           const int sg0 = ch * p.segs_per_chunk;
           const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
           if (!cfirst) mbar_wait(&S.cempty[sc], pc ^ 1);
-          if (p.dbg & 32) {
-            mbar_arrive(&S.cfull[sc]);
-          } else {
-            mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
-            for (int q = sg0; q < sg1; ++q)
-              bulk_g2s_hint(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB,
-                            S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[sc], evict_first);
-          }
+          mbar_arrive_expect_tx(&S.cfull[sc], (uint32_t)(sg1 - sg0) * CB);
+          for (int q = sg0; q < sg1; ++q)
+            bulk_g2s_hint(ring + p.co + (size_t)sc * p.cbytes + (size_t)(q - sg0) * CB,
+                          S.segs[q].codes + (size_t)unit * CB, CB, &S.cfull[sc], evict_first);
           if (++sc == p.nc) { sc = 0; pc ^= 1; cfirst = false; }
         }
         if (has_w) {
@@ -752,17 +748,15 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             MESW_PROF(tq = clock64();)
             tc_fence_after();
             const uint64_t wd = wdesc0 + (uint64_t)(sw * wstride);
-            if (!(p.dbg & 8)) {
-              mma2_ss_w(d_base, wd, xd, id_base, f0);
+            mma2_ss_w(d_base, wd, xd, id_base, f0);
 #pragma unroll
-              for (int j = 1; j < 8; ++j) mma2_ss_w(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
-            }
+            for (int j = 1; j < 8; ++j) mma2_ss_w(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
             tc2_commit_w(&S.wempty[sw]);
             if (++sw == p.nw) { sw = 0; pw ^= 1; }
             MESW_PROF(prof[2] += clock64() - tq;)
           }
           for (int q = 0; q < p.n_seg; ++q) {
-            if (!(p.dbg & 16) && S.seg_iss[q] == role) {
+            if (S.seg_iss[q] == role) {
               MESW_PROF(tq = clock64();)
               mbar_wait_cluster(&S.afull[abase_own + aslot], aph);
               MESW_PROF(prof[3] += clock64() - tq;)
@@ -775,11 +769,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + (abase_own + aslot) * kAColsPerSlot);
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
               const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
-              if (!(p.dbg & 2)) {
-                mma2_ts_w(dd, a0, bd, id, f0);
+              mma2_ts_w(dd, a0, bd, id, f0);
 #pragma unroll
-                for (int j = 1; j < 8; ++j) mma2_ts_w(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
-              }
+              for (int j = 1; j < 8; ++j) mma2_ts_w(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
               tc2_commit_w(&S.aempty[abase_own + aslot]);
               if (++aslot == na_own) { aslot = 0; aph ^= 1; }
               MESW_PROF(prof[4] += clock64() - tq;)
@@ -829,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           mbar_wait(&S.cfull[sc], pc);
           MESW_PROF(dprof[0] += clock64() - dq;)
           const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
-          for (int q = sg0; q < ((p.dbg & 16) ? sg0 : sg1); ++q) {
+          for (int q = sg0; q < sg1; ++q) {
             const int iss = S.seg_iss[q];
             const int pos = iss == 0 ? ps0 : (iss == 1 ? ps1 : ps2);
             const int use = iss == 0 ? us0 : (iss == 1 ? us1 : us2);
@@ -864,13 +856,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
 #pragma unroll
             for (int kh = 0; kh < 2; ++kh) {
               uint32_t r[32];
-              if (p.dbg & 1) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) r[i] = cw[kh * WPK + i % WPK];
-              } else {
-                dequant_chunk<DB>(&cw[kh * WPK], r);
-              }
-              if (!(p.dbg & 4)) tmem_st32(a0 + lane_addr + 32 * kh, r);
+              dequant_chunk<DB>(&cw[kh * WPK], r);
+              tmem_st32(a0 + lane_addr + 32 * kh, r);
             }
             MESW_PROF(dprof[2] += clock64() - dq;)
             MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 2] = clock64();)
@@ -915,8 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       const bool fast = gather_salient_x(p, S, cg, gtid);
       EpiPre pre;
       epi_prefetch(p, S, cg, mrow, 0, fast, pre);
-      if (p.dbg & 128) mbar_wait(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
-      else mbar_wait_sleep(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
+      mbar_wait_sleep(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
       tc_fence_after();
       if (gtid == 0 && pi == po.np - 1) MESW_STAMP(5);
       const uint32_t acc = tbase + lane_addr + (uint32_t)(ab * 2 * NP);
