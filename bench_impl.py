@@ -155,14 +155,15 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
     stream = torch.cuda.current_stream()
     # device-resident timing: the serving engine's form -- expert groups on 16-row boundaries,
     # activations already in the canonical tile layout, one pre-built launch per replica
-    from paper_2406_09041_b200.device import LinearPlan, align_segments, pack_x
+    from paper_2406_09041_b200.device import LinearPlan, align_segments, corr_table, pack_x
     rows, asegs, src = align_segments(C1_B, segs)
     xa = torch.zeros((rows, C1_M), dtype=torch.bfloat16, device="cuda")
     src_t = torch.as_tensor(src, dtype=torch.int64, device="cuda")
     xa[src_t >= 0] = x[src_t[src_t >= 0]]
-    xc = pack_x(xa)
+    corr = corr_table(rows, C1_M, "cuda")  # offset-code bias table, written with the canonical x
+    xc = pack_x(xa, corr=corr)
     ya = torch.empty((rows, C1_N), dtype=torch.bfloat16, device="cuda")
-    plans = [LinearPlan(xc, rows, dw, table, asegs, ya) for dw, table in sets]
+    plans = [LinearPlan(xc, rows, dw, table, asegs, ya, x_corr=corr) for dw, table in sets]
 
     def step(i):
         plans[i % replicas]()
@@ -212,14 +213,14 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
     for i in range(args.warmup):
         xd.copy_(xh, non_blocking=True)
         dw, table = sets[i % replicas]
-        me_linear(xd, dw, table, segs, out=y)
+        me_linear(xd, dw, table, segs, out=y, offset_codes=True)
         yh.copy_(y, non_blocking=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(args.steps):
         xd.copy_(xh, non_blocking=True)
         dw, table = sets[i % replicas]
-        me_linear(xd, dw, table, segs, out=y)
+        me_linear(xd, dw, table, segs, out=y, offset_codes=True)
         yh.copy_(y, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e2e_s = (time.perf_counter() - t0) / args.steps
@@ -233,7 +234,7 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
                    "parallelism": f"expert-sharded replicas x{ws}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic("c1"), "peak_kind": peak_kind,
-                     "bytes_per_launch": bytes_launch, "kernel": "me_linear_tc_kernel<2> (cta_group::2 pairs)"},
+                     "bytes_per_launch": bytes_launch, "kernel": "me_linear_tc_kernel<2, true> (cta_group::2 pairs, offset-form codes)"},
         "e2e": {"value": ws * C1_B / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(xh.numel() * 2),
                 "d2h_bytes_per_step": int(yh.numel() * 2)},
         "gpu_launches": args.steps,

@@ -176,6 +176,14 @@ typedef struct {
   int32_t* counters;  /* >= n_pad/128 int32, zero before first use (self-resetting) */
   int32_t num_ctas;   /* 0 = one persistent CTA per SM                         */
   int32_t activation; /* 0: none, 1: ReLU (toylm.py:207), applied last         */
+  /* Optional (2-bit codes): per-token offset-code bias table written by the producer of
+   * x (mesw_pack_x / the decoder glue): x_corr[t * x_corr_ld + ks] = sum over the 128
+   * inputs k of k-step ks of w_k * x[t][k], w_k = 130, 34, 10 for ((k % 64) / 2) % 8 in
+   * {0,3,6}, {1,4,7}, {2,5} (rows t >= B: 0).  When given, codes expand with one
+   * instruction per word (c + u offset form) and the bias is removed in f32 in the
+   * epilogue (~1e-5 relative on the delta term); NULL: exact q expansion.          */
+  const float* x_corr;
+  int32_t x_corr_ld;
 } mesw_linear_args;
 
 /* Canonical activation layout consumed by mesw_me_linear: rows padded to
@@ -185,8 +193,10 @@ typedef struct {
  * (the UMMA K-major SWIZZLE_NONE canonical B operand), so one bulk copy per CTA stages it:
  *   index(t, k) = (k/128)*NP*128 + ((t/8)%2)*(NP/2)*128 + (t/16)*1024
  *                 + ((k%128)/8)*64 + (t%8)*8 + k%8.
- * Rows >= B and columns >= m are written as 0. */
-int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t* d_xc, void* stream);
+ * Rows >= B and columns >= m are written as 0.  d_corr (optional, NULL = none): also
+ * write the offset-code bias table of mesw_linear_args.x_corr for all NP rows. */
+int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t* d_xc, float* d_corr, int corr_ld,
+                void* stream);
 /* Inverse (debug / tests): canonical -> row-major [B][ldy]. */
 int mesw_unpack_x(const uint16_t* d_xc, int B, int m, uint16_t* d_y, int ldy, void* stream);
 
@@ -196,7 +206,8 @@ int mesw_me_linear(const mesw_linear_args* args, void* stream);
 
 /* Glue outputs: row-major with leading dimension ld, or -- when *_np > 0 -- the
  * canonical activation layout (see mesw_pack_x) with NP = *_np rows, ready to be
- * the x operand of the next fused linear. */
+ * the x operand of the next fused linear.  d_corr (optional, NULL = none): also write
+ * its offset-code bias table (mesw_linear_args.x_corr) with leading dimension corr_ld. */
 /* ------------------------------------- K5: Mistral decoder glue (decode step)
  * The reference toy model has no attention (toylm.py:1-8); these are the
  * standard decoder pieces around the fused linears of the Mistral-shaped
@@ -206,7 +217,7 @@ int mesw_embed(const int32_t* d_ids, int B, const uint16_t* d_table, int H, uint
                int ld_out, void* stream);
 /* y = x * rsqrt(mean(x^2) + eps) * w */
 int mesw_rmsnorm(const uint16_t* d_x, int ldx, const uint16_t* d_w, int B, int H, float eps,
-                 uint16_t* d_y, int ldy, int y_np, void* stream);
+                 uint16_t* d_y, int ldy, int y_np, float* d_corr, int corr_ld, void* stream);
 /* RoPE (rotate-half) on the q and k heads of a fused qkv row, append k/v to the
  * caches [B][ctx_max][n_kv][head_dim] at position pos[b]. */
 int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_pos, int B, int n_heads,
@@ -219,10 +230,11 @@ uint64_t mesw_attention_workspace_bytes(int B, int n_heads, int ctx_max);
 int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
                           const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
                           int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
-                          int out_np, void* workspace, uint64_t workspace_bytes, void* stream);
+                          int out_np, void* workspace, uint64_t workspace_bytes, float* d_corr,
+                          int corr_ld, void* stream);
 /* out = silu(gate) * up for rows [gate(I) | up(I)]. */
 int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,
-                int out_np, void* stream);
+                int out_np, float* d_corr, int corr_ld, void* stream);
 /* Greedy next token: argmax with ties to the lowest id (toylm.py:247). */
 int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int ld, int32_t* d_out,
                 void* stream);

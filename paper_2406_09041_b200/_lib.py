@@ -36,7 +36,8 @@ class LinearArgs(C.Structure):
                 ("seg_slot", C.c_int32 * MAX_SEGMENTS), ("y", C.c_void_p), ("y_bf16", C.c_int32),
                 ("ldy", C.c_int32), ("residual", C.c_void_p), ("ld_res", C.c_int32),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
-                ("counters", C.c_void_p), ("num_ctas", C.c_int32), ("activation", C.c_int32)]
+                ("counters", C.c_void_p), ("num_ctas", C.c_int32), ("activation", C.c_int32),
+                ("x_corr", C.c_void_p), ("x_corr_ld", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/mesw.h
@@ -66,21 +67,21 @@ _SIGNATURES = [
                                      C.c_void_p]),
     ("mesw_unpack_weight_debug", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                            C.c_uint32, C.c_void_p, C.c_void_p]),
-    ("mesw_pack_x", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    ("mesw_pack_x", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_unpack_x", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_linear_workspace_bytes", C.c_uint64, [C.c_int32, C.c_int32]),
     ("mesw_me_linear", C.c_int, [C.POINTER(LinearArgs), C.c_void_p]),
     ("mesw_embed", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_rmsnorm", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p,
-                               C.c_int, C.c_int, C.c_void_p]),
+                               C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_rope_append", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_float, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_attention_workspace_bytes", C.c_uint64, [C.c_int, C.c_int, C.c_int]),
     ("mesw_attention_decode", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                         C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
-                                        C.c_void_p, C.c_uint64, C.c_void_p]),
+                                        C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_swiglu", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int,
-                              C.c_void_p]),
+                              C.c_void_p, C.c_int, C.c_void_p]),
     ("mesw_argmax", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     ("mesw_compress_workspace_bytes", C.c_uint64, [C.c_uint32, C.c_uint32]),
     ("mesw_compress_layer", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32,

@@ -20,6 +20,21 @@ __device__ __forceinline__ size_t canon_index(int t, int k, int NP) {
 }
 
 // Output address of element (t, k): row-major with ld, or canonical when np > 0.
+// Offset-code bias weight of input k (mesw.h x_corr): pair l = ((k % 64) / 2) % 8 ->
+// 130 (l in {0,3,6}), 34 ({1,4,7}), 10 ({2,5}).
+__device__ __forceinline__ float corr_w(int k) {
+  const int l = ((k & 63) >> 1) & 7;
+  const int m = l < 6 ? l % 3 : l - 6;
+  return m == 0 ? 130.f : (m == 1 ? 34.f : 10.f);
+}
+
+// sum over the 16-lane half-warp holding one k-step (fixed tree order: deterministic)
+__device__ __forceinline__ float sum16(float v) {
+#pragma unroll
+  for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ size_t out_index(int t, int k, int ld, int np) {
   return np > 0 ? canon_index(t, k, np) : (size_t)t * ld + k;
 }
@@ -73,7 +88,8 @@ constexpr int kNormThreads = 256;
 constexpr int kNormMaxVec = 4;  // up to 256 * 4 * 8 = 8192 channels
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* __restrict__ x, int ldx,
                                                                const uint16_t* __restrict__ w, int H, float eps,
-                                                               uint16_t* __restrict__ y, int ldy, int ynp) {
+                                                               uint16_t* __restrict__ y, int ldy, int ynp,
+                                                               float* __restrict__ corr, int corr_ld) {
   pdl_trigger();
   pdl_wait();  // inputs may come from the previous kernel in the stream
   __shared__ float red[32];
@@ -96,6 +112,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
 #pragma unroll
   for (int j = 0; j < kNormMaxVec; ++j) {
     const int i = threadIdx.x + j * kNormThreads;
+    float c = 0.f;
     if (i < nvec) {
       const uint4 g4 = wr[i];
       const uint32_t* e = reinterpret_cast<const uint32_t*>(&v[j]);
@@ -108,6 +125,12 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
         oo[q] = *reinterpret_cast<uint32_t*>(&t);
       }
       *reinterpret_cast<uint4*>(y + out_index(blockIdx.x, i * 8, ldy, ynp)) = o;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c += corr_w(i * 8 + 2 * q) * (bf16_lo(oo[q]) + bf16_hi(oo[q]));
+    }
+    if (corr) {  // 16 consecutive threads hold the 16 chunks of one k-step (H % 128 == 0)
+      c = sum16(c);
+      if (i < nvec && (i & 15) == 0) corr[(size_t)blockIdx.x * corr_ld + i / 16] = c;
     }
   }
 }
@@ -253,7 +276,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
 // Merge the splits of one (request, head): out = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s.
 __global__ void __launch_bounds__(128) attn_merge_kernel(const float* __restrict__ part, const int32_t* __restrict__ len,
                                                          int n_heads, int S, uint16_t* __restrict__ out, int ld_out,
-                                                         int out_np) {
+                                                         int out_np, float* __restrict__ corr, int corr_ld) {
+  __shared__ float red[4];
   pdl_trigger();
   pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
@@ -267,23 +291,46 @@ __global__ void __launch_bounds__(128) attn_merge_kernel(const float* __restrict
     den = fmaf(w, pp[(size_t)s2 * kAttnPart + 1], den);
     num = fmaf(w, pp[(size_t)s2 * kAttnPart + 2 + d], num);
   }
-  out[out_index(b, h * 128 + d, ld_out, out_np)] = __bfloat16_as_ushort(__float2bfloat16_rn(num / den));
+  const __nv_bfloat16 ob = __float2bfloat16_rn(num / den);
+  out[out_index(b, h * 128 + d, ld_out, out_np)] = __bfloat16_as_ushort(ob);
+  if (corr) {  // one head = one k-step of o_proj
+    float c = corr_w(d) * __bfloat162float(ob);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((d & 31) == 0) red[d >> 5] = c;
+    __syncthreads();
+    if (d == 0) corr[(size_t)b * corr_ld + h] = (red[0] + red[1]) + (red[2] + red[3]);
+  }
 }
 
 // out = silu(gate) * up, gate/up halves of a [B][2I] row.
 __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int ld_gu, int I, uint16_t* __restrict__ out,
-                              int ld_out, int out_np) {
+                              int ld_out, int out_np, float* __restrict__ corr, int corr_ld) {
   pdl_trigger();
   pdl_wait();  // inputs may come from the previous kernel in the stream
+  // 4 outputs per thread: a warp covers 128 consecutive outputs = one k-step of the next linear
   const int b = blockIdx.y;
   const uint16_t* r = gu + (size_t)b * ld_gu;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2; i < I; i += gridDim.x * blockDim.x * 2) {
-    const uint32_t g2 = *reinterpret_cast<const uint32_t*>(r + i);
-    const uint32_t u2 = *reinterpret_cast<const uint32_t*>(r + I + i);
-    const float g0 = bf16_lo(g2), g1 = bf16_hi(g2);
-    const float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
-    *reinterpret_cast<__nv_bfloat162*>(out + out_index(b, i, ld_out, out_np)) =
-        __floats2bfloat162_rn(s0 * bf16_lo(u2), s1 * bf16_hi(u2));
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4; i < I; i += gridDim.x * blockDim.x * 4) {
+    const uint2 g4 = *reinterpret_cast<const uint2*>(r + i);
+    const uint2 u4 = *reinterpret_cast<const uint2*>(r + I + i);
+    const uint32_t gg[2] = {g4.x, g4.y}, uu[2] = {u4.x, u4.y};
+    uint32_t o[2];
+    float c = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float g0 = bf16_lo(gg[h]), g1 = bf16_hi(gg[h]);
+      const float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
+      __nv_bfloat162 v = __floats2bfloat162_rn(s0 * bf16_lo(uu[h]), s1 * bf16_hi(uu[h]));
+      o[h] = *reinterpret_cast<uint32_t*>(&v);
+      c += corr_w(i + 2 * h) * (bf16_lo(o[h]) + bf16_hi(o[h]));
+    }
+    *reinterpret_cast<uint2*>(out + out_index(b, i, ld_out, out_np)) = make_uint2(o[0], o[1]);
+    if (corr) {
+#pragma unroll
+      for (int q = 16; q; q >>= 1) c += __shfl_xor_sync(0xffffffffu, c, q);
+      if ((threadIdx.x & 31) == 0) corr[(size_t)b * corr_ld + i / 128] = c;
+    }
   }
 }
 
@@ -327,12 +374,12 @@ __global__ void argmax_kernel(const void* __restrict__ logits, int is_bf16, int 
 
 // Row-major -> canonical (one thread per 16-byte chunk of 8 k); zero padding.
 __global__ void pack_x_kernel(const uint16_t* __restrict__ x, int B, int m, int ldx, uint16_t* __restrict__ xc,
-                              int NP, int n_ks) {
+                              int NP, int n_ks, float* __restrict__ corr, int corr_ld) {
   pdl_trigger();
   pdl_wait();  // inputs may come from the previous kernel in the stream
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)n_ks * NP * 16;
-  if (tid >= total) return;
+  if (tid >= total) return;  // (total is a multiple of 16: k-step groups never straddle the exit)
   const int kc = (int)(tid % 16);
   const int t = (int)((tid / 16) % NP);
   const int ks = (int)(tid / (16LL * NP));
@@ -350,6 +397,14 @@ __global__ void pack_x_kernel(const uint16_t* __restrict__ x, int B, int m, int 
     }
   }
   *reinterpret_cast<uint4*>(xc + canon_index(t, k0, NP)) = v;
+  if (corr) {
+    const uint32_t* e = reinterpret_cast<const uint32_t*>(&v);
+    float c = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c += corr_w(k0 + 2 * q) * (bf16_lo(e[q]) + bf16_hi(e[q]));
+    c = sum16(c);
+    if (kc == 0) corr[(size_t)t * corr_ld + ks] = c;
+  }
 }
 
 __global__ void unpack_x_kernel(const uint16_t* __restrict__ xc, int B, int m, int NP, uint16_t* __restrict__ y,
@@ -395,11 +450,13 @@ extern "C" int mesw_embed(const int32_t* d_ids, int B, const uint16_t* d_table, 
 }
 
 extern "C" int mesw_rmsnorm(const uint16_t* d_x, int ldx, const uint16_t* d_w, int B, int H, float eps,
-                            uint16_t* d_y, int ldy, int y_np, void* stream) {
+                            uint16_t* d_y, int ldy, int y_np, float* d_corr, int corr_ld, void* stream) {
+  if (d_corr && (H % 128 || corr_ld < H / 128)) return mesw_fail(MESW_ERR_VALUE, "rmsnorm: corr table needs H % 128 == 0");
   if (B <= 0 || H % 8 || H > kNormThreads * kNormMaxVec * 8 || ldx % 8 || ldy % 8)
     return mesw_fail(MESW_ERR_VALUE, "rmsnorm: H and strides must be multiples of 8, H <= 8192");
   if (y_np > 0 && (y_np % 16 || y_np < B)) return mesw_fail(MESW_ERR_VALUE, "rmsnorm: canonical rows must be >= B, multiple of 16");
-  mesw_launch(rmsnorm_kernel, dim3(B), dim3(kNormThreads), 0, (cudaStream_t)stream, d_x, ldx, d_w, H, eps, d_y, ldy, y_np);
+  mesw_launch(rmsnorm_kernel, dim3(B), dim3(kNormThreads), 0, (cudaStream_t)stream, d_x, ldx, d_w, H, eps, d_y, ldy, y_np,
+              d_corr, corr_ld);
   return mesw_check_launch("rmsnorm");
 }
 
@@ -420,7 +477,8 @@ extern "C" uint64_t mesw_attention_workspace_bytes(int B, int n_heads, int ctx_m
 extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
                                      const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
                                      int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
-                                     int out_np, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+                                     int out_np, void* d_workspace, uint64_t workspace_bytes, float* d_corr,
+                                     int corr_ld, void* stream) {
   if (B <= 0 || n_kv <= 0 || n_heads % n_kv || ctx_max <= 0) return mesw_fail(MESW_ERR_VALUE, "attention: bad shape");
   if (head_dim != 128) return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: head_dim must be 128");
   if (!d_workspace || workspace_bytes < mesw_attention_workspace_bytes(B, n_heads, ctx_max))
@@ -441,17 +499,20 @@ extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16
       return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: heads per kv head must be 1, 2, 4 or 8");
   }
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
+  if (d_corr && corr_ld < n_heads) return mesw_fail(MESW_ERR_VALUE, "attention: corr_ld too small");
   e = mesw_launch(attn_merge_kernel, dim3(B, n_heads), dim3(128), 0, s, (const float*)part, d_len, n_heads, S, d_out,
-                  ld_out, out_np);
+                  ld_out, out_np, d_corr, corr_ld);
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("attention_decode");
 }
 
 extern "C" int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,
-                           int out_np, void* stream) {
-  if (B <= 0 || I % 2) return mesw_fail(MESW_ERR_VALUE, "swiglu: bad shape");
-  dim3 grid((I / 2 + 255) / 256 < 64 ? (I / 2 + 255) / 256 : 64, B);
-  mesw_launch(swiglu_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, d_gu, ld_gu, I, d_out, ld_out, out_np);
+                           int out_np, float* d_corr, int corr_ld, void* stream) {
+  if (B <= 0 || I % 128 || ld_gu % 4 || (out_np == 0 && ld_out % 4)) return mesw_fail(MESW_ERR_VALUE, "swiglu: I must be a multiple of 128");
+  if (d_corr && corr_ld < I / 128) return mesw_fail(MESW_ERR_VALUE, "swiglu: corr_ld too small");
+  dim3 grid((I / 4 + 255) / 256 < 64 ? (I / 4 + 255) / 256 : 64, B);
+  mesw_launch(swiglu_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, d_gu, ld_gu, I, d_out, ld_out, out_np,
+              d_corr, corr_ld);
   return mesw_check_launch("swiglu");
 }
 
@@ -462,11 +523,14 @@ extern "C" int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int 
   return mesw_check_launch("argmax");
 }
 
-extern "C" int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t* d_xc, void* stream) {
+extern "C" int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t* d_xc, float* d_corr, int corr_ld,
+                           void* stream) {
   if (B <= 0 || m <= 0 || ldx < m) return mesw_fail(MESW_ERR_VALUE, "pack_x: bad shape");
   const int NP = (B + 15) & ~15, n_ks = (m + 127) / 128;
   const long long total = (long long)n_ks * NP * 16;
-  mesw_launch(pack_x_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, d_x, B, m, ldx, d_xc, NP, n_ks);
+  if (d_corr && corr_ld < n_ks) return mesw_fail(MESW_ERR_VALUE, "pack_x: corr_ld too small");
+  mesw_launch(pack_x_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, d_x, B, m, ldx, d_xc,
+              NP, n_ks, d_corr, corr_ld);
   return mesw_check_launch("pack_x");
 }
 

@@ -96,6 +96,8 @@ struct LinearParams {
   // it can never alias a phase two steps away.
   int a_base[3], a_na[3];
   int ring_bytes;  // dynamic shared memory past the Smem header
+  const float* x_corr;  // offset-code bias table [t * x_corr_ld + ks] (OFF kernels)
+  int x_corr_ld;
   int n_iss;  // MMA issuer threads (a tcgen05.mma stream runs ~60-85 cycles/instr per issuer)
   unsigned long long* tbuf;  // MESW_TIMING: per-CTA globaltimer stamps
   int dbg;  // reserved (MESW_DBG)
@@ -116,6 +118,7 @@ struct Smem {
   int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
   int8_t seg_iss[MESW_MAX_SEGMENTS];                         // MMA issuer of each segment
   float xsal[kMaxRows][kSalFast];  // x[t][salient idx r] of the current column group (fast path)
+  float corr[kMaxRows];             // offset codes: per-token bias over the piece's k range
 };
 
 __host__ __device__ inline size_t ring_offset() { return (sizeof(Smem) + 1023) & ~size_t(1023); }
@@ -327,6 +330,28 @@ __device__ __forceinline__ void dequant_chunk<2>(const uint32_t* cw, uint32_t* r
     o[5] = bf16x2_fma(lop3_and_or(b, 0x00300030u, 0x43004300u), 0x3D803D80u, 0xC120C120u);
     o[6] = bf16x2_fma(lop3_and_or(c, 0x00030003u, 0x43004300u), 0x3F803F80u, 0xC302C302u);
     o[7] = bf16x2_fma(lop3_and_or(c, 0x000C000Cu, 0x43004300u), 0x3E803E80u, 0xC208C208u);
+  }
+}
+
+// 2-bit codes in offset form, one lop3 per bf16x2 word: the magic exponent is chosen per
+// bit position so the result is the exact bf16 value c_l + u (c_l = 128, 32, 8 for code bits
+// 0-1, 2-3, 4-5 of the mantissa) -- no rescaling fma.  The MMA accumulates
+// sum_k (c_k + u_k) x_k = sum_k q_k x_k + sum_k (c_k + 2) x_k; the second term comes per
+// (token, k-step) from the table the activation's producer wrote (mesw.h x_corr) and is
+// subtracted in f32 in the epilogue.
+__device__ __forceinline__ void dequant_chunk2_offset(const uint32_t* cw, uint32_t* r) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t a = cw[w], b = a >> 6, c = a >> 12;
+    uint32_t* o = r + 8 * w;
+    o[0] = lop3_and_or(a, 0x00030003u, 0x43004300u);
+    o[1] = lop3_and_or(a, 0x000C000Cu, 0x42004200u);
+    o[2] = lop3_and_or(a, 0x00300030u, 0x41004100u);
+    o[3] = lop3_and_or(b, 0x00030003u, 0x43004300u);
+    o[4] = lop3_and_or(b, 0x000C000Cu, 0x42004200u);
+    o[5] = lop3_and_or(b, 0x00300030u, 0x41004100u);
+    o[6] = lop3_and_or(c, 0x00030003u, 0x43004300u);
+    o[7] = lop3_and_or(c, 0x000C000Cu, 0x42004200u);
   }
 }
 
@@ -558,7 +583,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // its own TMEM, and drains its own accumulators; the leader (rank 0) issues all MMAs and
 // commits them to both CTAs' barriers (multicast).  The peer relays its "tile landed"
 // events to the leader's barriers.
-template <int DB>
+template <int DB, bool OFF>
 __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_constant__ LinearParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   Smem& S = *reinterpret_cast<Smem*>(smem);
@@ -856,7 +881,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
 #pragma unroll
             for (int kh = 0; kh < 2; ++kh) {
               uint32_t r[32];
-              dequant_chunk<DB>(&cw[kh * WPK], r);
+              if (OFF) dequant_chunk2_offset(&cw[kh * WPK], r);
+              else dequant_chunk<DB>(&cw[kh * WPK], r);
               tmem_st32(a0 + lane_addr + 32 * kh, r);
             }
             MESW_PROF(dprof[2] += clock64() - dq;)
@@ -900,6 +926,16 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       const long long cg_end = (long long)(cgp + 1) * p.n_ks;
       const bool whole = (u == (long long)cgp * p.n_ks) && (piece_end == cg_end);
       const bool fast = gather_salient_x(p, S, cg, gtid);
+      if (OFF) {  // offset-code bias of each token over this piece's k-steps (table: 4 B / token / k-step)
+        const int ks0 = (int)(u - (long long)cgp * p.n_ks), ks1 = (int)(piece_end - (long long)cgp * p.n_ks);
+        for (int t = gtid; t < NP; t += 128) {
+          const float* row = p.x_corr + (size_t)t * p.x_corr_ld;
+          float acc = 0.f;
+          for (int ks = ks0; ks < ks1; ++ks) acc += __ldg(row + ks);
+          S.corr[t] = acc;
+        }
+        named_bar_sync(1, 128);
+      }
       EpiPre pre;
       epi_prefetch(p, S, cg, mrow, 0, fast, pre);
       mbar_wait_sleep(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
@@ -922,6 +958,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             const int dw = (t0 - sd.win0) / 2;  // window's column inside the expert's D range
             tmem_ld8(acc + (uint32_t)(NP + sd.win0 + dw), vd);
             tmem_ld8(acc + (uint32_t)(NP + sd.win0 + sd.winN / 2 + dw), vd + 8);
+            if (OFF) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) vd[i] -= S.corr[t0 + i];  // offset-code bias
+            }
           } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) vd[i] = 0.f;
@@ -952,7 +992,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             tmem_ld8(acc + (uint32_t)(NP + sd.win0 + sd.winN / 2 + dw), vd + 8);
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (pre.sg >= 0 && S.tok2seg[t0 + i] == pre.sg) vb[i] = fmaf(pre.sj, vd[i], vb[i]);
+              if (pre.sg >= 0 && S.tok2seg[t0 + i] == pre.sg)
+                vb[i] = fmaf(pre.sj, OFF ? vd[i] - S.corr[t0 + i] : vd[i], vb[i]);
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) __stcg(mine + (size_t)(t0 + i) * kUnitN + mrow, vb[i]);
@@ -1074,11 +1115,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   }
 }
 
-template <int DB>
+template <int DB, bool OFF>
 int launch(const LinearParams& p, size_t smem, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(me_linear_tc_kernel<DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(me_linear_tc_kernel<DB, OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          232448);
     if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
     configured = true;
@@ -1097,7 +1138,7 @@ int launch(const LinearParams& p, size_t smem, cudaStream_t stream) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = mesw_pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, me_linear_tc_kernel<DB>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, me_linear_tc_kernel<DB, OFF>, p);
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("me_linear");
 }
@@ -1165,6 +1206,10 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   if (p.n_cg % 2) return mesw_fail(MESW_ERR_VALUE, "device buffers must cover an even number of 128-column groups");
   p.T = (long long)(p.n_cg / 2) * p.n_ks;  // pair units (2 column groups x 1 k-step)
   p.activation = a->activation;
+  p.x_corr = (a->n_segments > 0 && a->code_bits == 2) ? a->x_corr : nullptr;
+  p.x_corr_ld = a->x_corr_ld;
+  if (p.x_corr && p.x_corr_ld < p.n_ks)
+    return mesw_fail(MESW_ERR_VALUE, "x_corr_ld must cover the k-steps of the linear");
   {
     const char* e = getenv("MESW_DBG");
     p.dbg = e ? atoi(e) : 0;
@@ -1274,8 +1319,8 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
 
   cudaStream_t s = (cudaStream_t)stream;
   switch (db) {
-    case 2: return launch<2>(p, smem, s);
-    case 4: return launch<4>(p, smem, s);
-    default: return launch<8>(p, smem, s);
+    case 2: return p.x_corr ? launch<2, true>(p, smem, s) : launch<2, false>(p, smem, s);
+    case 4: return launch<4, false>(p, smem, s);
+    default: return launch<8, false>(p, smem, s);
   }
 }

@@ -301,14 +301,27 @@ def canonical_numel(B: int, m: int) -> int:
     return _ceil(m) * canonical_rows(B)
 
 
-def pack_x(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """Row-major bf16 [B, m] -> canonical tile layout (include/mesw.h, mesw_pack_x)."""
+def corr_table(B: int, m: int, device) -> torch.Tensor:
+    """Zeroed offset-code bias table [canonical_rows(B), ceil(m/128)] f32 (mesw.h x_corr)."""
+    return torch.zeros((canonical_rows(B), _ceil(m) // 128), dtype=torch.float32, device=device)
+
+
+def pack_x(x: torch.Tensor, out: torch.Tensor | None = None, stream=None,
+           corr: torch.Tensor | None = None) -> torch.Tensor:
+    """Row-major bf16 [B, m] -> canonical tile layout (include/mesw.h, mesw_pack_x);
+    optionally also the offset-code bias table `corr` (corr_table)."""
     if x.dtype != torch.bfloat16 or x.dim() != 2 or not x.is_cuda or x.stride(1) != 1:
         raise ValueError("x must be a row-contiguous 2-D bf16 CUDA tensor")
     B, m = x.shape
     if out is None:
         out = torch.empty(canonical_numel(B, m), dtype=torch.bfloat16, device=x.device)
-    _lib.check(_lib.lib().mesw_pack_x(x.data_ptr(), B, m, x.stride(0), out.data_ptr(), _stream(stream)))
+    cp, cld = 0, 0
+    if corr is not None:
+        if corr.dtype != torch.float32 or not corr.is_contiguous() or tuple(corr.shape) != (canonical_rows(B), _ceil(m) // 128):
+            raise ValueError("corr must be a contiguous f32 [canonical_rows(B), ceil(m/128)] tensor")
+        cp, cld = corr.data_ptr(), corr.stride(0)
+    _lib.check(_lib.lib().mesw_pack_x(x.data_ptr(), B, m, x.stride(0), out.data_ptr(), cp or None, cld,
+                                      _stream(stream)))
     return out
 
 
@@ -329,7 +342,8 @@ class LinearPlan:
 
     def __init__(self, xc: torch.Tensor, B: int, weight: DeviceWeight | None, table: ExpertTable | None,
                  segments, out: torch.Tensor, residual: torch.Tensor | None = None,
-                 geom: LinearGeometry | None = None, num_ctas: int = 0, activation: str | None = None):
+                 geom: LinearGeometry | None = None, num_ctas: int = 0, activation: str | None = None,
+                 x_corr: torch.Tensor | None = None):
         L = _lib.lib()
         if geom is None:
             geom = weight.geom if weight is not None else next(
@@ -348,7 +362,7 @@ class LinearPlan:
         if len(segs) > _lib.MAX_SEGMENTS:
             raise NotImplementedError(f"more than {_lib.MAX_SEGMENTS} expert segments in one launch")
         self.geom = geom
-        self.keep = (xc, weight, table, out, residual)  # keep buffers alive
+        self.keep = (xc, weight, table, out, residual, x_corr)  # keep buffers alive
         ws = Workspace.get(xc.device)
         self.ws = ws
         a = _lib.LinearArgs()
@@ -371,6 +385,11 @@ class LinearPlan:
         a.counters = ws.counters.data_ptr()
         a.num_ctas = num_ctas
         a.activation = {None: 0, "relu": 1}[activation]
+        if x_corr is not None:  # offset-code bias table written with xc (2-bit codes only)
+            if (x_corr.dtype != torch.float32 or not x_corr.is_contiguous() or x_corr.dim() != 2
+                    or x_corr.shape[0] < canonical_rows(B) or x_corr.shape[1] < _ceil(geom.m) // 128):
+                raise ValueError("x_corr must be a contiguous f32 [canonical_rows(B), ceil(m/128)] tensor")
+            a.x_corr, a.x_corr_ld = x_corr.data_ptr(), x_corr.stride(0)
         self.args = a
         self._fn = L.mesw_me_linear
 
@@ -400,8 +419,12 @@ def align_segments(B: int, segments) -> tuple:
 def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
               segments, out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
               out_dtype=torch.bfloat16, geom: LinearGeometry | None = None, num_ctas: int = 0,
-              activation: str | None = None, stream=None) -> torch.Tensor:
+              activation: str | None = None, stream=None, offset_codes: bool = False) -> torch.Tensor:
     """y = x.W + x.Dtilde_{expert(t)} (+ residual) -- the fused kernel on row-major inputs.
+
+    offset_codes: pass the activation bias table so 2-bit codes expand in offset form
+    (mesw.h x_corr; the bf16 serving engine's choice, ~1e-5 relative on the delta term).
+    The default keeps the exact q expansion (the f32 provider path holds 1e-4).
 
     x: bf16 [B, >= m] on the GPU, rows grouped by expert; segments: iterable of
     (begin, end, slot) into `table`.  The rows are packed into the canonical layout;
@@ -418,8 +441,9 @@ def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable |
     segs = [(int(b), int(e), int(s)) for b, e, s in segments]
     xm = x[:, :geom.m] if x.shape[1] >= geom.m else x
     if all(b % 16 == 0 for b, _, _ in segs) and B <= MAX_ROWS:
-        xc = pack_x(xm.contiguous() if xm.stride(1) != 1 else xm, stream=stream)
-        LinearPlan(xc, B, weight, table, segs, out, residual, geom, num_ctas, activation)(stream)
+        corr = corr_table(B, geom.m, x.device) if offset_codes else None
+        xc = pack_x(xm.contiguous() if xm.stride(1) != 1 else xm, stream=stream, corr=corr)
+        LinearPlan(xc, B, weight, table, segs, out, residual, geom, num_ctas, activation, x_corr=corr)(stream)
         return out
     rows, new_segs, src = align_segments(B, segs)
     cuts, start = [], 0
@@ -443,8 +467,9 @@ def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable |
         if weight is None and not csegs:
             yp.zero_()
         else:
-            xc = pack_x(xp, stream=stream)
+            corr = corr_table(n_rows, geom.m, x.device) if offset_codes else None
+            xc = pack_x(xp, stream=stream, corr=corr)
             LinearPlan(xc, n_rows, weight, table if csegs else None, csegs, yp, rp, geom, num_ctas,
-                       activation)(stream)
+                       activation, x_corr=corr)(stream)
         out[src_t[valid]] = yp[valid]
     return out

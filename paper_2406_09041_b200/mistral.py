@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan, _stream,
-                     canonical_numel, canonical_rows)
+                     canonical_numel, canonical_rows, corr_table)
 from .synth import MistralShape
 
 PROJ_ORDER = ("q", "k", "v", "o", "gate", "up", "down")
@@ -62,8 +62,9 @@ class MistralMultiExpert:
     """Base model + resident experts + decode buffers for up to `max_batch` requests."""
 
     def __init__(self, shape: MistralShape = MistralShape(), max_batch: int = 64, ctx_max: int = 256,
-                 device="cuda", n_layers: int | None = None):
+                 device="cuda", n_layers: int | None = None, offset_codes: bool = True):
         self.shape = shape
+        self.offset_codes = offset_codes  # 2-bit codes in offset form + glue-written bias tables
         self.n_layers = shape.n_layers if n_layers is None else n_layers
         self.device = torch.device(device)
         self.max_batch = max_batch
@@ -261,15 +262,20 @@ class MistralMultiExpert:
                 "attn": torch.zeros(canonical_numel(rows, self.g_o.m), dtype=torch.bfloat16, device=self.device),
                 "act": torch.zeros(canonical_numel(rows, self.g_down.m), dtype=torch.bfloat16, device=self.device),
             }
+            # offset-code bias tables written by the glue next to each canonical input (mesw.h x_corr)
+            for k, m in (("xn", s.hidden), ("attn", self.g_o.m), ("act", self.g_down.m)):
+                bufs[k + "_corr"] = corr_table(rows, m, self.device) if self.offset_codes else None
             h, qkv, gu = self.h[r0:r1], self.qkv[r0:r1], self.gu[r0:r1]
             layers = []
             for l, lw in enumerate(self.layers):
                 tq, to, tgu, td = self.tables[l]
                 layers.append((
-                    LinearPlan(bufs["xn"], rows, lw.qkv, tq if segs else None, segs, qkv),
-                    LinearPlan(bufs["attn"], rows, lw.o, to if segs else None, segs, h, residual=h),
-                    LinearPlan(bufs["xn"], rows, lw.gateup, tgu if segs else None, segs, gu),
-                    LinearPlan(bufs["act"], rows, lw.down, td if segs else None, segs, h, residual=h),
+                    LinearPlan(bufs["xn"], rows, lw.qkv, tq if segs else None, segs, qkv, x_corr=bufs["xn_corr"]),
+                    LinearPlan(bufs["attn"], rows, lw.o, to if segs else None, segs, h, residual=h,
+                               x_corr=bufs["attn_corr"]),
+                    LinearPlan(bufs["xn"], rows, lw.gateup, tgu if segs else None, segs, gu, x_corr=bufs["xn_corr"]),
+                    LinearPlan(bufs["act"], rows, lw.down, td if segs else None, segs, h, residual=h,
+                               x_corr=bufs["act_corr"]),
                 ))
             head = LinearPlan(bufs["xn"], rows, self.head, None, [], self.logits[r0:r1])
             gplans.append((r0, r1, bufs, layers, head))
@@ -292,12 +298,16 @@ class MistralMultiExpert:
         def rows_ptr(t, r0):
             return t.data_ptr() + r0 * t.stride(0) * bf
 
+        def corr(bufs, k):  # (pointer, leading dimension) of a bias table, or none
+            c = bufs[k + "_corr"]
+            return (c.data_ptr(), c.stride(0)) if c is not None else (None, 0)
+
         chk(L.mesw_embed(self.ids.data_ptr(), B, self.embedding.data_ptr(), H, self.h.data_ptr(),
                          self.h.stride(0), st))
         for l, lw in enumerate(self.layers):
             for (r0, r1, bufs, layers, _) in self._plans:
                 chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), lw.attn_norm.data_ptr(), r1 - r0, H, eps,
-                                   bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+                                   bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "xn"), st))
                 layers[l][0](stream)
             kc, vc = self.kcache[l], self.vcache[l]
             chk(L.mesw_rope_append(self.qkv.data_ptr(), self.qkv.stride(0), self.pos.data_ptr(), B, s.n_heads,
@@ -308,19 +318,19 @@ class MistralMultiExpert:
                                             rows_ptr(vc, r0), self.len.data_ptr() + 4 * r0, r1 - r0, s.n_heads,
                                             s.n_kv_heads, s.head_dim, self.ctx_max, bufs["attn"].data_ptr(), 0,
                                             canonical_rows(r1 - r0), self.attn_ws.data_ptr(), self.attn_ws.numel(),
-                                            st))
+                                            *corr(bufs, "attn"), st))
                 layers[l][1](stream)
             for (r0, r1, bufs, layers, _) in self._plans:
                 chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), lw.mlp_norm.data_ptr(), r1 - r0, H, eps,
-                                   bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+                                   bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "xn"), st))
                 layers[l][2](stream)
             for (r0, r1, bufs, layers, _) in self._plans:
                 chk(L.mesw_swiglu(rows_ptr(self.gu, r0), self.gu.stride(0), r1 - r0, s.intermediate,
-                                  bufs["act"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+                                  bufs["act"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "act"), st))
                 layers[l][3](stream)
         for (r0, r1, bufs, _, head) in self._plans:
             chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), self.final_norm.data_ptr(), r1 - r0, H, eps,
-                               bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), st))
+                               bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), None, 0, st))
             head(stream)
         chk(L.mesw_argmax(self.logits.data_ptr(), 1, B, s.vocab, self.logits.stride(0), self.ids.data_ptr(), st))
         chk(L.mesw_advance_positions(self.pos.data_ptr(), self.len.data_ptr(), B, self.ctx_max,

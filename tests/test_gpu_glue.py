@@ -27,7 +27,7 @@ def test_attention_decode_matches_numpy(lens, G, ctx_max):
     s = torch.cuda.current_stream()
     _lib.check(L.mesw_attention_decode(tq.data_ptr(), tq.stride(0), tk.data_ptr(), tv.data_ptr(), tl.data_ptr(), B,
                                        n_heads, n_kv, D, ctx_max, out.data_ptr(), out.stride(0), 0, ws.data_ptr(),
-                                       ws.numel(), C.c_void_p(s.cuda_stream)))
+                                       ws.numel(), None, 0, C.c_void_p(s.cuda_stream)))
     got = out.float().cpu().numpy()
     qb, kb, vb = tq.float().cpu().numpy(), tk.float().cpu().numpy(), tv.float().cpu().numpy()
     ref = np.zeros_like(got)
@@ -42,4 +42,4 @@ def test_attention_decode_matches_numpy(lens, G, ctx_max):
     with pytest.raises(ValueError):
         _lib.check(L.mesw_attention_decode(tq.data_ptr(), tq.stride(0), tk.data_ptr(), tv.data_ptr(), tl.data_ptr(),
                                            B, n_heads, n_kv, D, ctx_max, out.data_ptr(), out.stride(0), 0,
-                                           ws.data_ptr(), 16, C.c_void_p(s.cuda_stream)))
+                                           ws.data_ptr(), 16, None, 0, C.c_void_p(s.cuda_stream)))

@@ -147,13 +147,18 @@ def test_fused_linear_matches_oracle(B, segs, num_ctas):
     geom, dw, w_bf, table, experts = _setup_linear(384, (256, 128), 3, seed=B)
     rng = np.random.default_rng(100 + B)
     x = torch.from_numpy(rng.normal(0, 1, size=(B, geom.m_pad)).astype(np.float32)).to(torch.bfloat16).cuda()
-    y = me_linear(x, dw, table, segs, out_dtype=torch.float32, num_ctas=num_ctas).cpu().numpy()
     ref = _oracle_linear(x.float().cpu().numpy()[:, :geom.m], w_bf, experts, segs, geom, B)
-    assert _rel(y, ref) <= 2e-3
-    # bf16 output + residual epilogue
     res = torch.from_numpy(rng.normal(0, 1, size=(B, geom.n)).astype(np.float32)).to(torch.bfloat16).cuda()
-    y2 = me_linear(x, dw, table, segs, residual=res, num_ctas=num_ctas).float().cpu().numpy()
-    assert _rel(y2, ref + res.float().cpu().numpy()) <= 1e-2
+    ys = []
+    for offset in (False, True):  # exact q expansion / offset form + bias table (mesw.h x_corr)
+        y = me_linear(x, dw, table, segs, out_dtype=torch.float32, num_ctas=num_ctas,
+                      offset_codes=offset).cpu().numpy()
+        assert _rel(y, ref) <= 2e-3
+        ys.append(y)
+        # bf16 output + residual epilogue
+        y2 = me_linear(x, dw, table, segs, residual=res, num_ctas=num_ctas, offset_codes=offset).float().cpu().numpy()
+        assert _rel(y2, ref + res.float().cpu().numpy()) <= 1e-2
+    assert _rel(ys[1], ys[0]) <= 1e-5  # the bias removal costs only f32 rounding
 
 
 @pytest.mark.parametrize("bits", [1, 3, 4, 8])

@@ -14,7 +14,7 @@ import torch
 
 from paper_2406_09041_b200 import compress, synth
 from paper_2406_09041_b200.device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan,
-                                           align_segments, pack_x)
+                                           align_segments, corr_table, pack_x)
 
 
 def make(m, n, E, seed):
@@ -31,7 +31,7 @@ def make(m, n, E, seed):
     return geom, dw, table
 
 
-def run(m, n, E, B, reps, base=True, replicas=3, num_ctas=0):
+def run(m, n, E, B, reps, base=True, replicas=3, num_ctas=0, offset=True):
     """Times the kernel alone: expert groups are laid out on 16-row boundaries (as the
     serving engine does) and each launch is a pre-built LinearPlan."""
     sets = [make(m, n, E, r) for r in range(replicas)]
@@ -43,10 +43,11 @@ def run(m, n, E, B, reps, base=True, replicas=3, num_ctas=0):
         cur += c
     rows, asegs, _ = align_segments(B, segs)
     x = (torch.randn((rows, m), device="cuda")).to(torch.bfloat16)
-    xc = pack_x(x)
+    corr = corr_table(rows, m, "cuda") if offset else None
+    xc = pack_x(x, corr=corr)
     y = torch.empty((rows, n), dtype=torch.bfloat16, device="cuda")
     plans = [LinearPlan(xc, rows, dw if base else None, table if E else None, asegs, y, geom=geom,
-                        num_ctas=num_ctas) for geom, dw, table in sets]
+                        num_ctas=num_ctas, x_corr=corr) for geom, dw, table in sets]
 
     for i in range(5):
         plans[i % replicas]()
@@ -59,7 +60,7 @@ def run(m, n, E, B, reps, base=True, replicas=3, num_ctas=0):
     torch.cuda.synchronize()
     us = st.elapsed_time(en) * 1e3 / reps
     nbytes = synth.linear_bytes(m, n, E, B, base=base)
-    print(f"m={m} n={n} E={E} B={B} rows={rows} base={base} ctas={num_ctas}: {us:8.2f} us  "
+    print(f"m={m} n={n} E={E} B={B} rows={rows} base={base} ctas={num_ctas} off={int(offset)}: {us:8.2f} us  "
           f"{nbytes/us/1e3:8.1f} GB/s ({nbytes/us/1e3/6549.8*100:5.1f}% of 6549.8)", flush=True)
 
 
@@ -72,6 +73,8 @@ if __name__ == "__main__":
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--ab", action="store_true")
     a = ap.parse_args()
     if a.sweep:
         for (m, n) in [(4096, 14336), (4096, 6144), (4096, 4096), (14336, 4096), (4096, 28672)]:
@@ -81,5 +84,10 @@ if __name__ == "__main__":
             run(4096, 14336, 3, B, a.reps)
         run(4096, 14336, 16, 32, a.reps)
         run(4096, 14336, 3, 8, a.reps, base=False)
+    elif a.ab:  # exact vs offset-form code expansion on the headline shapes
+        for (m, n, E, B) in [(4096, 14336, 3, 8), (4096, 6144, 3, 32), (14336, 4096, 3, 32), (4096, 28672, 3, 32),
+                             (4096, 4096, 3, 32), (4096, 14336, 16, 64)]:
+            run(m, n, E, B, a.reps, offset=False)
+            run(m, n, E, B, a.reps, offset=True)
     else:
-        run(a.m, a.n, a.experts, a.batch, a.reps, num_ctas=a.ctas)
+        run(a.m, a.n, a.experts, a.batch, a.reps, num_ctas=a.ctas, offset=not a.exact)
