@@ -162,7 +162,7 @@ def run_c2(args, ws, rank, local, ClockSampler, peaks):
                    "parallelism": f"expert-sharded replicas x{ws} (replicated base, no collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": f"me_linear_tc_kernel<2> (all {n_lin} fused linear launches of a step)",
+                     "kernel": f"me_linear_tc_kernel<2, true> (all {n_lin} fused linear launches of a step)",
                      "bytes_per_step": lin_bytes, "kernel_ms_per_step": lin_ms,
                      "kernel_share_of_step": lin_ms / per_step},
         "delta_gemm": {"bytes_per_step": nbytes["delta"],
