@@ -24,6 +24,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-re
          "-I", os.path.join(ROOT, "include")]
 if os.environ.get("MESW_PROFILE"):  # role-loop cycle counters for tools/ktiming.py (rebuild with --force)
     FLAGS.append("-DMESW_PROFILE")
+FLAGS += os.environ.get("MESW_XFLAGS", "").split()  # experiment switches (-D...), rebuild with --force
 
 
 def sources():

@@ -255,6 +255,32 @@ int mesw_compress_layer(const float* d_delta, uint32_t m, uint32_t n, const floa
                         uint16_t* d_sal_rows, uint8_t* d_packed, void* d_workspace,
                         uint64_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------ f3: step-size distillation
+ * The per-layer pieces of compress.distill_step_sizes (compress.py:331-378); the model
+ * forward / backward around them are plain f32 GEMMs (host side, distill.py).  Given the
+ * same inputs each is bit-exact with the reference's numpy (f64 order kept, no FMA).
+ * row_slot int32[m]: -1 for quantized rows, r >= 0 for salient row r (rows f32[k][n],
+ * fp16-rounded values); NULL = no salient rows.
+ * QuantizedLayerState.reconstruct (toylm.py:379-384), optionally fused with `w + d`
+ * (toylm.py:422-424): out = (base ? base : 0) + reconstruction.                   */
+int mesw_ste_reconstruct(const float* d_delta, uint32_t m, uint32_t n, const float* d_steps, uint32_t bits,
+                         const int32_t* d_row_slot, const float* d_sal_rows, const float* d_base,
+                         float* d_out, void* stream);
+/* QuantizedLayerState.step_gradient -> quant.ste_step_gradient (toylm.py:386-391,
+ * quant.py:142-169): grad f32[n] from upstream f32[m][n] (salient rows masked). */
+int mesw_ste_step_grad(const float* d_delta, uint32_t m, uint32_t n, const float* d_steps, uint32_t bits,
+                       const int32_t* d_row_slot, const float* d_upstream, float* d_grad, void* stream);
+/* _Adam.step for one step vector (compress.py:288-302; f64 moments d_m/d_v, weight
+ * decay 0) followed by the clamp max(steps, step_floor) (compress.py:375).
+ * bias_corr1/2 = 1 - beta1**t, 1 - beta2**t (computed by the caller in f64). */
+int mesw_adam_step(float* d_steps, double* d_m, double* d_v, const float* d_grad, uint32_t n, double lr,
+                   double beta1, double beta2, double eps, double bias_corr1, double bias_corr2,
+                   float step_floor, void* stream);
+/* compress._repack (compress.py:325-335): codes of the unmasked rows re-derived from
+ * the trained steps (salient_mask u8[m] != 0 -> code 0), packed like mesw_compress_layer. */
+int mesw_quantize_pack(const float* d_delta, uint32_t m, uint32_t n, const float* d_steps, uint32_t bits,
+                       const uint8_t* d_salient_mask, uint8_t* d_packed, void* stream);
+
 /* ------------------------------------------------ K4: model-level router
  * Replaces SPEC router.classify for a batch of B queries:
  * multinomial Naive Bayes over FNV-1a-hashed character 2/3-grams (2^16 buckets),

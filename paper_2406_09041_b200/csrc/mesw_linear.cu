@@ -566,6 +566,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // Cycle-count profiling of the role loops (tools/ktiming.py): compiled in only with
 // -DMESW_PROFILE (MESW_PROFILE=1 python build.py --force); zero cost otherwise.
+#ifndef MESW_EXP_KH
+#define MESW_EXP_KH 2  // experiment switch: k-halves dequantized per job (2 = correct)
+#endif
 #ifdef MESW_PROFILE
 #define MESW_PROF(...) __VA_ARGS__
 #else
@@ -794,9 +797,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + (abase_own + aslot) * kAColsPerSlot);
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
               const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
+#ifndef MESW_EXP_NOMMA
               mma2_ts_w(dd, a0, bd, id, f0);
 #pragma unroll
               for (int j = 1; j < 8; ++j) mma2_ts_w(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
+#endif
               tc2_commit_w(&S.aempty[abase_own + aslot]);
               if (++aslot == na_own) { aslot = 0; aph ^= 1; }
               MESW_PROF(prof[4] += clock64() - tq;)
@@ -878,13 +883,15 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             MESW_PROF(dprof[1] += clock64() - dq;)
             MESW_PROF(dq = clock64();)
             const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
+#ifndef MESW_EXP_NODQ
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {
+            for (int kh = 0; kh < MESW_EXP_KH; ++kh) {
               uint32_t r[32];
               if (OFF) dequant_chunk2_offset(&cw[kh * WPK], r);
               else dequant_chunk<DB>(&cw[kh * WPK], r);
               tmem_st32(a0 + lane_addr + 32 * kh, r);
             }
+#endif
             MESW_PROF(dprof[2] += clock64() - dq;)
             MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 2] = clock64();)
             MESW_PROF(dq = clock64();)
@@ -931,7 +938,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
         for (int t = gtid; t < NP; t += 128) {
           const float* row = p.x_corr + (size_t)t * p.x_corr_ld;
           float acc = 0.f;
-          for (int ks = ks0; ks < ks1; ++ks) acc += __ldg(row + ks);
+#pragma unroll 8
+          for (int ks = ks0; ks < ks1; ++ks) acc += __ldg(row + ks);  // loads batched, adds in order
           S.corr[t] = acc;
         }
         named_bar_sync(1, 128);

@@ -4,21 +4,23 @@ os.environ["MESW_TIMING"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2406_09041_b200 import _lib
-from paper_2406_09041_b200.device import LinearPlan, pack_x
+from paper_2406_09041_b200.device import LinearPlan, corr_table, pack_x
 from kbench import make
 L = _lib.lib()
 L.mesw_debug_timing_copy.argtypes = [C.c_void_p, C.c_int]
 m, n = int(sys.argv[1]), int(sys.argv[2])
 E, rows = int(sys.argv[3]), int(sys.argv[4])
-geom, dw, table = make(m, n, max(E, 1), 0)
+sets = [make(m, n, max(E, 1), r) for r in range(3)]  # rotate replicas: the timed launch is HBM-cold
 segs = [(16 * i, 16 * i + 3, i) for i in range(E)] if E else []
 rows = max(rows, 16 * (E - 1) + 3) if E else rows
 x = torch.randn((rows, m), device="cuda").to(torch.bfloat16)
 y = torch.empty((rows, n), dtype=torch.bfloat16, device="cuda")
-plan = LinearPlan(pack_x(x), rows, dw, table if E else None, segs, y, geom=geom)
-for _ in range(3): plan()
+corr = corr_table(rows, m, "cuda") if os.environ.get("EXACT") is None else None
+xc = pack_x(x, corr=corr)
+plans = [LinearPlan(xc, rows, dw, table if E else None, segs, y, geom=geom, x_corr=corr) for geom, dw, table in sets]
+for i in range(6): plans[i % 3]()
 torch.cuda.synchronize()
-plan(); torch.cuda.synchronize()
+plans[0](); torch.cuda.synchronize()
 G = min(148, (n // 128) * (m // 128))
 G -= G % 2
 buf = np.zeros(60 * 4096, np.uint64)
@@ -36,6 +38,14 @@ for i, nm in enumerate(names):
     if v.size:
         print(f"  {nm:12s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f}")
 
+# per-CTA phase durations (us): differences within one CTA, so clock skew between SMs cancels
+pairs = [("start->mma_done", 0, 3), ("mma_done->accfull", 3, 5), ("accfull->tmem", 5, 6), ("tmem->epi_end", 6, 7),
+         ("epi_end->synced", 7, 1), ("synced->fin", 1, 2), ("fin->red_done", 2, 4)]
+for nm, a_, b_ in pairs:
+    ok = (t[:, a_] > 0) & (t[:, b_] > 0)
+    if ok.any():
+        d = (t[ok, b_] - t[ok, a_]) / 1e3
+        print(f"  {nm:18s} med {np.median(d):7.2f}  min {d.min():7.2f}  max {d.max():7.2f}  n={ok.sum()}")
 pm = ["wait_x", "wait_w", "base_issue", "wait_afull", "delta_issue", "unit_sum", "total", "jobs"]
 pd = ["wait_cfull", "wait_aempty", "dequant+st", "wait_st+arrive", "-", "-", "total", "jobs"]
 lead = prof[0::2, 0, :]
