@@ -163,7 +163,13 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
     corr = corr_table(rows, C1_M, "cuda")  # offset-code bias table, written with the canonical x
     xc = pack_x(xa, corr=corr)
     ya = torch.empty((rows, C1_N), dtype=torch.bfloat16, device="cuda")
-    plans = [LinearPlan(xc, rows, dw, table, asegs, ya, x_corr=corr) for dw, table in sets]
+    from paper_2406_09041_b200.device import Workspace, cta_candidates, tune_num_ctas
+    dw0, tab0 = sets[0]
+    scratch = torch.empty_like(ya)
+    ctas = tune_num_ctas(("c1", rows, tuple(asegs)), lambda c: LinearPlan(xc, rows, dw0, tab0, asegs, scratch,
+                                                                       x_corr=corr, num_ctas=c),
+                         cta_candidates(dw0.geom, Workspace.get("cuda").sms))
+    plans = [LinearPlan(xc, rows, dw, table, asegs, ya, x_corr=corr, num_ctas=ctas) for dw, table in sets]
 
     def step(i):
         plans[i % replicas]()
@@ -241,6 +247,7 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
         "clocks": clk.summary(),
     }
     line["config"]["rows_padded"] = rows
+    line["config"]["num_ctas"] = ctas or "all SMs"  # launch width chosen by device.tune_num_ctas
     if rank == 0 and not args.no_cpu_baseline:
         dt, n = cpu_c1_baseline()
         line["cpu_baseline"] = {"value": C1_B / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",

@@ -561,7 +561,7 @@ __device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& 
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");  // not hoisted across barriers
   return t;
 }
 // Cycle-count profiling of the role loops (tools/ktiming.py): compiled in only with
@@ -576,6 +576,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 #define MESW_STAMP(i) \
   do { if (p.tbuf) p.tbuf[(size_t)blockIdx.x * 8 + (i)] = gtimer(); } while (0)
+// second stamp bank (tail phases), tools/ktiming.py
+#define MESW_STAMP2(i) \
+  do { if (p.tbuf) p.tbuf[4096 + (size_t)blockIdx.x * 8 + (i)] = gtimer(); } while (0)
 
 // ---------------------------------------------------------------- kernel
 // A cluster of two CTAs ("pair") owns two adjacent column groups (256 output channels)
@@ -1024,9 +1027,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
         const long long first_u = (long long)cgp * p.n_ks, last_u = first_u + p.n_ks - 1;
         const int p_first = unit_owner(first_u, T2, (int)G2), p_last = unit_owner(last_u, T2, (int)G2);
         if (gtid == 0) {
+          if (pi == po.np - 1) MESW_STAMP2(0);
           // acq_rel: releases this CTA's partials (ordered by the barrier) and, for the last
           // arriver, acquires every other contributor's (their release increments)
           const int prev = atom_add_acq_rel_gpu(&p.counters[cg], 1);
+          if (pi == po.np - 1) MESW_STAMP2(1);
           S.flag = (prev == p_last - p_first) ? 1 : 0;
         }
         named_bar_sync(1, 128);
@@ -1057,6 +1062,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) MESW_STAMP(1);
+  if (threadIdx.x == kEpiWarp0 * 32) MESW_STAMP2(2);
   if (S.fin.on) {  // this CTA is the last contributor of its final column group (acquired above)
     if (threadIdx.x == 0) MESW_STAMP(2);
     const int fcg = S.fin.cg, fcgp = S.fin.cgp, pf = S.fin.p_first, pl = S.fin.p_last;
@@ -1095,6 +1101,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           }
         }
         mbar_wait(&S.finbar, ph);
+        if (threadIdx.x == 0 && done == 0) MESW_STAMP2(3);
         ph ^= 1;
         for (int i = 1; i < region0 + cnt; ++i)
           for (size_t e = threadIdx.x; e < slot_floats; e += kThreads) st[e] += st[(size_t)i * slot_floats + e];
@@ -1103,6 +1110,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       }
     }
     MESW_PROF(fp[1] += clock64() - fq; fq = clock64();)
+    if (threadIdx.x == 0) MESW_STAMP2(4);
     for (int t0 = t_first; t0 < NP; t0 += 16 * (kThreads / kUnitN)) {
       EpiPre pre;
       if (t0 == t_first) pre = pre0;
@@ -1116,7 +1124,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     if (threadIdx.x == 0) p.counters[S.fin.cg] = 0;
     if (threadIdx.x == 0) MESW_STAMP(4);
   }
+  if (threadIdx.x == 0) MESW_STAMP2(5);
   cluster_sync_all();  // the peer's MMAs / TMEM reads are complete before deallocation
+  if (threadIdx.x == 0) MESW_STAMP2(6);
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));

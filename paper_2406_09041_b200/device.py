@@ -397,6 +397,58 @@ class LinearPlan:
         _lib.check(self._fn(C.byref(self.args), _stream(stream)))
 
 
+# ------------------------------------------------------------------ launch-width tuning
+# K2 splits (column-group pair, k-step) units over CTA pairs (stream-K).  When the units
+# divide evenly into whole column groups or aligned k-splits, the final reduction has
+# fewer contributors and the launch tail shrinks (measured: o_proj 4096x4096 B=32 E=3
+# 33.3 us on 148 CTAs -> 27.6 us on 128), while for ALU-heavy expert mixes every SM
+# counts.  The best width depends on shape and expert mix, so plans are timed once per
+# shape key and the winner cached (tune_num_ctas).
+
+_TUNED: dict = {}
+
+
+def cta_candidates(geom: "LinearGeometry", sms: int) -> list:
+    """Even CTA counts worth timing for a linear: all SMs, a few narrower grids, and the
+    widest grid whose pairs each own an aligned k-split of one column-group pair."""
+    g2max = sms // 2
+    n_cgp = (geom.n_pad + 255) // 256
+    n_ks = geom.m_pad // TILE
+    cands = {0}
+    for f in (0.97, 0.86, 0.75):
+        cands.add(2 * max(1, int(g2max * f)))
+    best = 0
+    for s_ in range(1, n_ks + 1):
+        if n_ks % s_ == 0 and n_cgp * s_ <= g2max:
+            best = s_
+    if best:
+        cands.add(2 * n_cgp * best)
+    return sorted(c for c in cands if c <= sms)
+
+
+def tune_num_ctas(key, make_plan, candidates, reps: int = 8, stream=None) -> int:
+    """Time `make_plan(num_ctas)()` for each candidate (CUDA events, after warm-up) and
+    cache the fastest under `key`.  make_plan must build plans on scratch outputs."""
+    if key in _TUNED:
+        return _TUNED[key]
+    best, best_t = 0, None
+    for c in candidates:
+        plan = make_plan(c)
+        for _ in range(2):
+            plan(stream)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for _ in range(reps):
+            plan(stream)
+        en.record()
+        en.synchronize()
+        t = st.elapsed_time(en)
+        if best_t is None or t < best_t:
+            best, best_t = c, t
+    _TUNED[key] = best
+    return best
+
+
 def align_segments(B: int, segments) -> tuple:
     """Re-layout rows so every expert segment starts at a multiple of 16 rows (the
     kernel's tcgen05 N granularity).  Returns (rows_pad, new_segments, src) where

@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan, _stream,
-                     canonical_numel, canonical_rows, corr_table)
+                     Workspace, canonical_numel, canonical_rows, corr_table, cta_candidates, tune_num_ctas)
 from .synth import MistralShape
 
 PROJ_ORDER = ("q", "k", "v", "o", "gate", "up", "down")
@@ -62,8 +62,9 @@ class MistralMultiExpert:
     """Base model + resident experts + decode buffers for up to `max_batch` requests."""
 
     def __init__(self, shape: MistralShape = MistralShape(), max_batch: int = 64, ctx_max: int = 256,
-                 device="cuda", n_layers: int | None = None, offset_codes: bool = True):
+                 device="cuda", n_layers: int | None = None, offset_codes: bool = True, tune: bool = True):
         self.shape = shape
+        self.tune = tune  # time candidate launch widths per linear kind once per batch layout
         self.offset_codes = offset_codes  # 2-bit codes in offset form + glue-written bias tables
         self.n_layers = shape.n_layers if n_layers is None else n_layers
         self.device = torch.device(device)
@@ -266,20 +267,40 @@ class MistralMultiExpert:
             for k, m in (("xn", s.hidden), ("attn", self.g_o.m), ("act", self.g_down.m)):
                 bufs[k + "_corr"] = corr_table(rows, m, self.device) if self.offset_codes else None
             h, qkv, gu = self.h[r0:r1], self.qkv[r0:r1], self.gu[r0:r1]
+            # per linear kind: (input, weight of layer l, table index, output, residual?)
+            kinds = (("qkv", "xn", lambda lw: lw.qkv, 0, qkv, False), ("o", "attn", lambda lw: lw.o, 1, h, True),
+                     ("gu", "xn", lambda lw: lw.gateup, 2, gu, False), ("down", "act", lambda lw: lw.down, 3, h, True))
+            ctas = {}
+            for name, xin, wsel, ti, out, res in kinds:
+                ctas[name] = self._tuned_ctas(name, rows, segs, bufs[xin], bufs[xin + "_corr"], wsel(self.layers[0]),
+                                              self.tables[0][ti] if segs else None, out, res)
             layers = []
             for l, lw in enumerate(self.layers):
-                tq, to, tgu, td = self.tables[l]
-                layers.append((
-                    LinearPlan(bufs["xn"], rows, lw.qkv, tq if segs else None, segs, qkv, x_corr=bufs["xn_corr"]),
-                    LinearPlan(bufs["attn"], rows, lw.o, to if segs else None, segs, h, residual=h,
-                               x_corr=bufs["attn_corr"]),
-                    LinearPlan(bufs["xn"], rows, lw.gateup, tgu if segs else None, segs, gu, x_corr=bufs["xn_corr"]),
-                    LinearPlan(bufs["act"], rows, lw.down, td if segs else None, segs, h, residual=h,
-                               x_corr=bufs["act_corr"]),
-                ))
-            head = LinearPlan(bufs["xn"], rows, self.head, None, [], self.logits[r0:r1])
+                tabs = self.tables[l]
+                layers.append(tuple(
+                    LinearPlan(bufs[xin], rows, wsel(lw), tabs[ti] if segs else None, segs, out,
+                               residual=out if res else None, x_corr=bufs[xin + "_corr"], num_ctas=ctas[name])
+                    for name, xin, wsel, ti, out, res in kinds))
+            head = LinearPlan(bufs["xn"], rows, self.head, None, [], self.logits[r0:r1],
+                              num_ctas=self._tuned_ctas("head", rows, [], bufs["xn"], None, self.head, None,
+                                                        self.logits[r0:r1], False))
             gplans.append((r0, r1, bufs, layers, head))
         self._plans = gplans
+
+    def _tuned_ctas(self, name, rows, segs, xc, corr, weight, table, out, res) -> int:
+        """Launch width of one linear kind for this batch layout, timed on scratch outputs
+        (device.tune_num_ctas; cached per shape key).  0 = one CTA per SM."""
+        if not self.tune:
+            return 0
+        key = ("mistral", name, self.shape, rows, tuple((b, e) for b, e, _ in segs),
+               table.code_bits if table is not None else 0, corr is not None)
+        scratch = torch.empty_like(out)
+
+        def make(c):
+            return LinearPlan(xc, rows, weight, table, segs, scratch, residual=scratch if res else None,
+                              x_corr=corr, num_ctas=c)
+        sms = Workspace.get(self.device).sms
+        return tune_num_ctas(key, make, cta_candidates(weight.geom, sms))
 
     def step(self, stream=None) -> None:
         """One decode step for the whole batch: ids (engine order) -> next ids in self.ids.

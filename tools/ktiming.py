@@ -46,6 +46,19 @@ for nm, a_, b_ in pairs:
     if ok.any():
         d = (t[ok, b_] - t[ok, a_]) / 1e3
         print(f"  {nm:18s} med {np.median(d):7.2f}  min {d.min():7.2f}  max {d.max():7.2f}  n={ok.sum()}")
+t2 = buf[4096:4096 + G * 8].reshape(G, 8).astype(np.int64)
+print("  tail (bank 2, per-CTA us):")
+for nm, (ba, a_), (bb, b_) in [("epi_end->pre_atomic", (0, 7), (1, 0)), ("atomic", (1, 0), (1, 1)),
+                               ("atomic->synced(epi)", (1, 1), (1, 2)), ("synced(t0)-synced(epi)", (1, 2), (0, 1)),
+                               ("fin->copies_landed", (0, 2), (1, 3)), ("copies->sums_done", (1, 3), (1, 4)),
+                               ("sums->reduced", (1, 4), (0, 4)), ("red_done->pre_cluster", (0, 4), (1, 5)),
+                               ("cluster_sync", (1, 5), (1, 6)), ("start->exit", (0, 0), (1, 6))]:
+    A = (t if ba == 0 else t2)[:, a_]
+    Bv = (t if bb == 0 else t2)[:, b_]
+    ok = (A > 0) & (Bv > 0)
+    if ok.any():
+        d = (Bv[ok] - A[ok]) / 1e3
+        print(f"    {nm:24s} med {np.median(d):7.2f}  min {d.min():7.2f}  max {d.max():7.2f}  n={ok.sum()}")
 pm = ["wait_x", "wait_w", "base_issue", "wait_afull", "delta_issue", "unit_sum", "total", "jobs"]
 pd = ["wait_cfull", "wait_aempty", "dequant+st", "wait_st+arrive", "-", "-", "total", "jobs"]
 lead = prof[0::2, 0, :]
