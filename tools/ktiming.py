@@ -48,17 +48,15 @@ for nm, a_, b_ in pairs:
         print(f"  {nm:18s} med {np.median(d):7.2f}  min {d.min():7.2f}  max {d.max():7.2f}  n={ok.sum()}")
 t2 = buf[4096:4096 + G * 8].reshape(G, 8).astype(np.int64)
 print("  tail (bank 2, per-CTA us):")
-for nm, (ba, a_), (bb, b_) in [("epi_end->pre_atomic", (0, 7), (1, 0)), ("atomic", (1, 0), (1, 1)),
-                               ("atomic->synced(epi)", (1, 1), (1, 2)), ("synced(t0)-synced(epi)", (1, 2), (0, 1)),
-                               ("fin->copies_landed", (0, 2), (1, 3)), ("copies->sums_done", (1, 3), (1, 4)),
-                               ("sums->reduced", (1, 4), (0, 4)), ("red_done->pre_cluster", (0, 4), (1, 5)),
-                               ("cluster_sync", (1, 5), (1, 6)), ("start->exit", (0, 0), (1, 6))]:
-    A = (t if ba == 0 else t2)[:, a_]
-    Bv = (t if bb == 0 else t2)[:, b_]
-    ok = (A > 0) & (Bv > 0)
+flag = t2[:, 7]
+print("    epilogue done when thread 0 passed the final barrier:", int((flag == 1001).sum()), "of", int((flag >= 1000).sum()))
+print("  tail (bank 2: SM clock cycles, per CTA):")
+for nm, a_, b_ in [("atomic", 0, 1), ("atomic->synced(epi)", 1, 2), ("synced->copies_landed", 2, 3),
+                   ("copies->summed", 3, 4), ("summed->reduced", 4, 5), ("cluster_sync", 5, 6)]:
+    ok = (t2[:, a_] > 0) & (t2[:, b_] > 0)
     if ok.any():
-        d = (Bv[ok] - A[ok]) / 1e3
-        print(f"    {nm:24s} med {np.median(d):7.2f}  min {d.min():7.2f}  max {d.max():7.2f}  n={ok.sum()}")
+        d = (t2[ok, b_] - t2[ok, a_])
+        print(f"    {nm:26s} med {np.median(d):9.0f}  min {d.min():9.0f}  max {d.max():9.0f}  n={ok.sum()}")
 pm = ["wait_x", "wait_w", "base_issue", "wait_afull", "delta_issue", "unit_sum", "total", "jobs"]
 pd = ["wait_cfull", "wait_aempty", "dequant+st", "wait_st+arrive", "-", "-", "total", "jobs"]
 lead = prof[0::2, 0, :]
