@@ -576,9 +576,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 #define MESW_STAMP(i) \
   do { if (p.tbuf) p.tbuf[(size_t)blockIdx.x * 8 + (i)] = gtimer(); } while (0)
-// second stamp bank (tail phases), tools/ktiming.py
+// second stamp bank (tail phases, SM clock cycles: %globaltimer reads of different warps of
+// one CTA were seen microseconds apart across a barrier), tools/ktiming.py
 #define MESW_STAMP2(i) \
-  do { if (p.tbuf) p.tbuf[4096 + (size_t)blockIdx.x * 8 + (i)] = gtimer(); } while (0)
+  do { if (p.tbuf) p.tbuf[4096 + (size_t)blockIdx.x * 8 + (i)] = (unsigned long long)clock64(); } while (0)
 
 // ---------------------------------------------------------------- kernel
 // A cluster of two CTAs ("pair") owns two adjacent column groups (256 output channels)
