@@ -1104,6 +1104,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
         mbar_wait(&S.finbar, ph);
         if (threadIdx.x == 0 && done == 0) MESW_STAMP2(3);
         ph ^= 1;
+        if (nC <= nbuf) break;  // all slots resident: summed in contributor order by reduce_chunk
         for (int i = 1; i < region0 + cnt; ++i)
           for (size_t e = threadIdx.x; e < slot_floats; e += kThreads) st[e] += st[(size_t)i * slot_floats + e];
         __syncthreads();
@@ -1116,7 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       EpiPre pre;
       if (t0 == t_first) pre = pre0;
       else epi_prefetch(p, S, fcg, fm, t0, ffast, pre);
-      if (staged) reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pf, ffast, pre, st);
+      if (staged) reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, nC <= nbuf ? pl : pf, ffast, pre, st);
       else reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre, nullptr);
       MESW_PROF(fp[2] += clock64() - fq; fq = clock64();)
     }
