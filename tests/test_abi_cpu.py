@@ -97,3 +97,16 @@ def test_salient_tables_layout():
                 jl = cg * 128 + c - cb
                 want = blocks[b].salient_rows.view(np.uint16)[rr, jl] if jl < blocks[b].n else 0
                 assert rows[r, c] == want
+
+
+def test_launch_width_candidates():
+    """device.cta_candidates: all-SM default, narrower grids, and the aligned k-split width."""
+    from paper_2406_09041_b200.device import LinearGeometry, cta_candidates
+    o_proj = LinearGeometry(4096, (4096,))       # 16 column-group pairs x 32 k-steps
+    c = cta_candidates(o_proj, 148)
+    assert c[0] == 0 and all(x % 2 == 0 and x <= 148 for x in c)
+    assert 128 in c                              # 16 pairs x 4 aligned k-splits = 64 pairs
+    down = LinearGeometry(14336, (4096,))        # 112 k-steps: 4 splits of 28
+    assert 128 in cta_candidates(down, 148)
+    gu = LinearGeometry(4096, (14336, 14336))    # 112 pairs > 74: no aligned split
+    assert all(x <= 148 for x in cta_candidates(gu, 148))
