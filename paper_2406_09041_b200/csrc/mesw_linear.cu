@@ -1231,9 +1231,10 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   if (p.x_corr && p.x_corr_ld < p.n_ks)
     return mesw_fail(MESW_ERR_VALUE, "x_corr_ld must cover the k-steps of the linear");
   {
-    const char* e = getenv("MESW_DBG");
+    static const char* e = getenv("MESW_DBG");  // experiment knobs: read once per process
     p.dbg = e ? atoi(e) : 0;
-    if (getenv("MESW_TIMING")) {
+    static const bool timing = getenv("MESW_TIMING") != nullptr;
+    if (timing) {
       if (!g_tbuf) cudaMalloc(&g_tbuf, 60 * 4096 * sizeof(unsigned long long)); cudaMemset(g_tbuf, 0, 60 * 4096 * 8);
       p.tbuf = g_tbuf;
     }
@@ -1297,10 +1298,12 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   // accumulator buffers, then more issuers.
   {
     int want = (p.w ? 1 : 0) + p.n_seg;
-    if (getenv("MESW_ISS")) want = std::min(want, atoi(getenv("MESW_ISS")));
+    static const int env_iss = getenv("MESW_ISS") ? atoi(getenv("MESW_ISS")) : 0;
+    if (env_iss > 0) want = std::min(want, env_iss);
     want = std::max(1, std::min(want, kMaxIssuers));
     bool done = false;
-    const int nacc_max = getenv("MESW_NACC") ? atoi(getenv("MESW_NACC")) : 2;
+    static const int nacc_max = getenv("MESW_NACC") ? atoi(getenv("MESW_NACC")) : 2;
+    static const int env_maxslots = getenv("MESW_MAXSLOTS") ? atoi(getenv("MESW_MAXSLOTS")) : 0;
     for (int n_acc = nacc_max; n_acc >= 1 && !done; --n_acc) {
       for (int iss = want; iss >= 1 && !done; --iss) {
         int n_delta = 0;  // issuers that own at least one segment
@@ -1312,7 +1315,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
         const int cols = kTmemCols - n_acc * 2 * p.NP;
         int slots = cols / kAColsPerSlot;
         if (slots > kMaxASlots) slots = kMaxASlots;
-        if (getenv("MESW_MAXSLOTS") && slots > atoi(getenv("MESW_MAXSLOTS"))) slots = atoi(getenv("MESW_MAXSLOTS"));
+        if (env_maxslots > 0 && slots > env_maxslots) slots = env_maxslots;
         if (cols < 0 || slots < n_delta) continue;
         // every issuer with delta jobs gets >= 1 slot; the rest go to the most loaded
         int jobs[3] = {0, 0, 0};

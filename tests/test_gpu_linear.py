@@ -236,9 +236,12 @@ def test_c1_shape_mixed_decode():
     x = torch.from_numpy(rng.normal(0, 1, size=(8, 4096)).astype(np.float32)).to(torch.bfloat16).cuda()
     # experts t mod 3 -> grouped order
     segs = [(0, 3, 0), (3, 6, 1), (6, 8, 2)]
-    y = me_linear(x, dw, table, segs, out_dtype=torch.float32).cpu().numpy()
     ref = _oracle_linear(x.float().cpu().numpy(), w_bf, experts, segs, geom, 8)
-    assert _rel(y, ref) <= 2e-3
+    # exact / offset-form codes, all SMs / the widths the tuner picks for this shape
+    for offset, ctas in ((False, 0), (True, 0), (True, 142), (True, 112)):
+        y = me_linear(x, dw, table, segs, out_dtype=torch.float32, offset_codes=offset,
+                      num_ctas=ctas).cpu().numpy()
+        assert _rel(y, ref) <= 2e-3, (offset, ctas)
 
 
 def test_pack_x_roundtrip_and_layout():
