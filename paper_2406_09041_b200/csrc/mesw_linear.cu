@@ -893,6 +893,13 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               uint32_t r[32];
               if (OFF) dequant_chunk2_offset(&cw[kh * WPK], r);
               else dequant_chunk<DB>(&cw[kh * WPK], r);
+#ifdef MESW_EXP_ST1  // experiment: expand both halves, store only the first (TMEM-store cost probe)
+              if (kh == 1) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) asm volatile("" ::"r"(r[i]));
+                continue;
+              }
+#endif
               tmem_st32(a0 + lane_addr + 32 * kh, r);
             }
 #endif
