@@ -415,7 +415,9 @@ def cta_candidates(geom: "LinearGeometry", sms: int) -> list:
     n_cgp = (geom.n_pad + 255) // 256
     n_ks = geom.m_pad // TILE
     cands = {0}
-    for f in (0.97, 0.86, 0.75):
+    for d in (1, 2, 3, 4, 6):      # just under the SM count (stream-K boundaries move)
+        cands.add(2 * (g2max - d))
+    for f in (0.86, 0.75):
         cands.add(2 * max(1, int(g2max * f)))
     best = 0
     for s_ in range(1, n_ks + 1):
@@ -426,7 +428,7 @@ def cta_candidates(geom: "LinearGeometry", sms: int) -> list:
     return sorted(c for c in cands if c <= sms)
 
 
-def tune_num_ctas(key, make_plan, candidates, reps: int = 8, stream=None) -> int:
+def tune_num_ctas(key, make_plan, candidates, reps: int = 16, stream=None) -> int:
     """Time `make_plan(num_ctas)()` for each candidate (CUDA events, after warm-up) and
     cache the fastest under `key`.  make_plan must build plans on scratch outputs."""
     if key in _TUNED:
