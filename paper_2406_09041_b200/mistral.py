@@ -247,8 +247,9 @@ class MistralMultiExpert:
         g = torch.Generator(device=self.device)
         g.manual_seed(seed)
         for t in (self.kcache, self.vcache):
-            view = t[:, :, :prompt_len]
-            view.copy_((torch.randn(view.shape, generator=g, device=self.device) * 0.5).to(torch.bfloat16))
+            for l in range(t.shape[0]):  # per layer: bounded temporaries (many-expert engines)
+                view = t[l, :, :prompt_len]
+                view.copy_((torch.randn(view.shape, generator=g, device=self.device) * 0.5).to(torch.bfloat16))
 
     # ------------------------------------------------------------------ step
     def _build_plans(self):
