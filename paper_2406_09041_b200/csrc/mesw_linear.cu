@@ -116,7 +116,6 @@ struct Smem {
   int tok2seg[kMaxRows];
   SegDesc segs[MESW_MAX_SEGMENTS];
   int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
-  int8_t seg_iss[MESW_MAX_SEGMENTS];                         // MMA issuer of each segment
   float xsal[kMaxRows][kSalFast];  // x[t][salient idx r] of the current column group (fast path)
   float corr[kMaxRows];             // offset codes: per-token bias over the piece's k range
 };
@@ -638,7 +637,6 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     d.winN = ((d.end + 15) & ~15) - d.begin;   // 16-token window(s)
     S.segs[q] = d;
     for (int t = d.begin; t < d.end; ++t) S.tok2seg[t] = q;
-    S.seg_iss[q] = (int8_t)seg_issuer(q, p.n_iss, p.w != nullptr);
   }
   tc_fence_before();
   __syncthreads();
@@ -742,6 +740,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       const uint32_t xstride = (uint32_t)p.xbytes >> 4, wstride = kUnitWBytes >> 4;
       const uint32_t id_base = idesc_bf16_m256(NP);
       const int na_own = p.a_na[role], abase_own = p.a_base[role];
+      const int iss_first = (has_w && p.n_iss > 1) ? 1 : 0;  // seg_issuer(q) = iss_first + q % q_step
+      const int q_step = p.n_iss - iss_first;
+      const int q_own0 = role >= iss_first ? role - iss_first : p.n_seg;
       int sx = 0, sw = 0;
       uint32_t px = 0, pw = 0;
       int aslot = 0;  // index within this issuer's sub-ring
@@ -787,8 +788,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             if (++sw == p.nw) { sw = 0; pw ^= 1; }
             MESW_PROF(prof[2] += clock64() - tq;)
           }
-          for (int q = 0; q < p.n_seg; ++q) {
-            if (S.seg_iss[q] == role) {
+          // this issuer's segments: seg_issuer() is round-robin, so stride through them
+          for (int q = q_own0; q < p.n_seg; q += q_step) {
+            {
               MESW_PROF(tq = clock64();)
               mbar_wait_cluster(&S.afull[abase_own + aslot], aph);
               MESW_PROF(prof[3] += clock64() - tq;)
@@ -840,6 +842,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     uint32_t pc = 0;
     // per issuer: position in its A sub-ring and completed laps (no divisions in the loop)
     int ps0 = 0, ps1 = 0, ps2 = 0, us0 = 0, us1 = 0, us2 = 0;
+    const int na0 = p.a_na[0], na1 = p.a_na[1], na2 = p.a_na[2];
+    const int ab0 = p.a_base[0], ab1 = p.a_base[1], ab2 = p.a_base[2];
+    const int iss_first = (has_w && p.n_iss > 1) ? 1 : 0, iss_last = p.n_iss - 1;
     MESW_PROF(long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
     MESW_PROF(const long long dstart = clock64();)
     MESW_PROF(int dcount = 0;)
@@ -848,6 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       long long pa, pb;
       po.bounds(pi, pa, pb);
       for (long long u = pa; u < pb; ++u) {
+        int q_iss = iss_first;  // issuer of segment 0
         for (int ch = 0; ch < p.n_chunks; ++ch) {
           const int sg0 = ch * p.segs_per_chunk;
           const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
@@ -856,18 +862,21 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           MESW_PROF(dprof[0] += clock64() - dq;)
           const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
           for (int q = sg0; q < sg1; ++q) {
-            const int iss = S.seg_iss[q];
+            const int iss = q_iss;  // == seg_issuer(q): register-only bookkeeping (no smem / indexed loads)
+            q_iss = q_iss == iss_last ? iss_first : q_iss + 1;
             const int pos = iss == 0 ? ps0 : (iss == 1 ? ps1 : ps2);
             const int use = iss == 0 ? us0 : (iss == 1 ? us1 : us2);
+            const int na_i = iss == 0 ? na0 : (iss == 1 ? na1 : na2);
+            const int ab_i = iss == 0 ? ab0 : (iss == 1 ? ab1 : ab2);
             {
-              const bool wrap = pos + 1 == p.a_na[iss];
+              const bool wrap = pos + 1 == na_i;
               const int np1 = wrap ? 0 : pos + 1, nu = use + (wrap ? 1 : 0);
               if (iss == 0) { ps0 = np1; us0 = nu; } else if (iss == 1) { ps1 = np1; us1 = nu; } else { ps2 = np1; us2 = nu; }
             }
             // slot-affine groups: A slot s is always filled by group s % 2 (whole jobs, both
             // k-halves: two independent dequant chains per thread), so every slot is written
             // by one group and read by one issuer, in sequence
-            const int aslot = p.a_base[iss] + pos;
+            const int aslot = ab_i + pos;
             if ((aslot & 1) != grp) continue;
             uint32_t cw[2 * WPK];
             const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
