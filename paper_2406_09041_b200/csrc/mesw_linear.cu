@@ -32,7 +32,10 @@
 
 namespace mesw {
 
-constexpr int kDqGroups = 2;  // dequant warpgroups: group g fills the A slots with parity g
+#ifndef MESW_DQ_GROUPS
+#define MESW_DQ_GROUPS 2
+#endif
+constexpr int kDqGroups = MESW_DQ_GROUPS;  // dequant warpgroups: group g fills the A slots s with s % kDqGroups == g
 // warp roles: 0 producer (codes, weight tiles, activations), 1-3 MMA issuers, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
 constexpr int kProdWarp = 0, kMmaWarp = 1;
 constexpr int kMaxIssuers = 3;  // warps 1..3
@@ -877,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             // k-halves: two independent dequant chains per thread), so every slot is written
             // by one group and read by one issuer, in sequence
             const int aslot = ab_i + pos;
-            if ((aslot & 1) != grp) continue;
+            if (aslot % kDqGroups != grp) continue;
             uint32_t cw[2 * WPK];
             const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
 #pragma unroll
