@@ -1347,6 +1347,12 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
           if (best < 0) break;
           p.a_na[best]++;
         }
+        // dequant groups are slot-affine (slot s -> group s % 2): an odd sub-ring of >= 3 slots
+        // hands one group more of that issuer's jobs (3 slots: 2/3 of them), so round it down
+        static const bool even_slots = getenv("MESW_ODD_SLOTS") == nullptr;
+        if (even_slots && kDqGroups == 2)
+          for (int i = 0; i < 3; ++i)
+            if (p.a_na[i] > 1 && (p.a_na[i] & 1)) p.a_na[i]--;
         int base = 0;
         for (int i = 0; i < 3; ++i) { p.a_base[i] = base; base += p.a_na[i]; }
         p.n_acc = n_acc;
