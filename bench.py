@@ -1,6 +1,6 @@
 """Benchmark driver (contract: one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|c4|c5]
 
 Workloads (BASELINE.json configs):
   c2 (default): full Mistral-7B-shaped decoder stack, 3 experts with 2-bit + fp16-salient
@@ -8,6 +8,8 @@ Workloads (BASELINE.json configs):
       for every request in the batch).
   c1: one 4096x14336 MLP linear, 3 experts, batch-8 mixed decode (the CPU-runnable case).
   c4: prefill of 2048 tokens over 16 experts through the same linear (tensor-bound roofline).
+  c5: 64 experts sharded over the N GPUs (64/N per GPU, expert e on rank e mod N), batch 128
+      per GPU through the c2 decode engine (with --gpus 1 all 64 experts are resident on one GPU).
 
 Under torchrun (N>1) every rank serves its own expert shard (experts placed e mod G,
 replicated base, no collective on the data path): weak scaling, value = all tokens / max time.
@@ -98,7 +100,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--experts", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

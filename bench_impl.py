@@ -358,4 +358,9 @@ def run_ours(args, ws, rank, local, ClockSampler, peaks):
     if args.config == "c1":
         return run_c1(args, ws, rank, local, ClockSampler, peaks)
     from bench_mistral import run_c2
+    if args.config == "c5":  # BASELINE configs[4]: 64 experts sharded over the ranks, replicated base
+        if 64 % ws:
+            raise ValueError("c5 shards 64 experts: --gpus must divide 64")
+        args.experts = 64 // ws
+        args.batch = args.batch or 128
     return run_c2(args, ws, rank, local, ClockSampler, peaks)

@@ -7,7 +7,7 @@ timeout 300 python bench.py --config c1 > gpurun_out/f_c1.log 2>&1
 timeout 600 python bench.py --experts 16 --batch 32 --no-cpu-baseline > gpurun_out/f_c3_32.log 2>&1
 timeout 600 python bench.py --experts 16 --batch 128 --no-cpu-baseline > gpurun_out/f_c3_128.log 2>&1
 timeout 300 python bench.py --config c4 > gpurun_out/f_c4.log 2>&1
-timeout 900 python bench.py --experts 64 --batch 128 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/f_c5.log 2>&1
+timeout 900 python bench.py --config c5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/f_c5.log 2>&1
 timeout 600 python bench.py --impl reference > gpurun_out/f_ref.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/f_smoke.log 2>&1
 # launch list of one decode step (C2, B=32, 3 experts), then one full capture of the C1 kernel
