@@ -232,6 +232,16 @@ int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcach
                           int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
                           int out_np, void* workspace, uint64_t workspace_bytes, float* d_corr,
                           int corr_ld, void* stream);
+/* Fused decode form of mesw_rope_append + mesw_attention_decode: d_qkv holds the new
+ * token's [q heads | k heads | v heads] row (not yet rotated), at position len[b] - 1
+ * (callers keep len = pos + 1).  Rotates q per split, rotates k and appends k / v to the
+ * caches from the split holding the new position, then attends as mesw_attention_decode.
+ * Same results, bit for bit, as the two-call form; one launch fewer per layer. */
+int mesw_attention_decode_rope(const uint16_t* d_qkv, int ld_qkv, uint16_t* d_kcache,
+                               uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
+                               int n_kv, int head_dim, float theta, int ctx_max, uint16_t* d_out,
+                               int ld_out, int out_np, void* workspace, uint64_t workspace_bytes,
+                               float* d_corr, int corr_ld, void* stream);
 /* out = silu(gate) * up for rows [gate(I) | up(I)]. */
 int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,
                 int out_np, float* d_corr, int corr_ld, void* stream);

@@ -186,10 +186,17 @@ constexpr int kAttnSplit = 64;     // positions per CTA
 constexpr int kAttnRow = 136;      // bf16 per staged row (128 + 8 pad: conflict-free row reads)
 constexpr int kAttnPart = 2 + 128; // floats per (b, head, split) partial: m, l, o[128]
 
-template <int G>
+// ROPE: fused decode form (rope_append folded in).  q holds the new token's fused qkv row
+// ([q heads | k heads | v heads], q and k not yet rotated); the new token sits at position
+// len[b] - 1 (the engine keeps len = pos + 1).  Every split rotates its q heads on load
+// (same arithmetic and bf16 rounding as rope_append_kernel); the split holding the new
+// position rotates k, stages the new k / v row from registers and appends it to the caches
+// (no other split reads that position in this launch).
+template <int G, bool ROPE>
 __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
-    const uint16_t* __restrict__ q, int ld_q, const uint16_t* __restrict__ kc, const uint16_t* __restrict__ vc,
-    const int32_t* __restrict__ len, int n_kv, int ctx_max, float scale, float* __restrict__ part, int S) {
+    const uint16_t* __restrict__ q, int ld_q, uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
+    const int32_t* __restrict__ len, int n_kv, int ctx_max, float scale, float* __restrict__ part, int S,
+    float theta) {
   pdl_trigger();
   pdl_wait();  // inputs may come from the previous kernel in the stream
   constexpr int D = 128;
@@ -205,13 +212,56 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
   const size_t kv_stride = (size_t)n_kv * D;
   const uint16_t* kb = kc + (((size_t)b * ctx_max + t0) * n_kv + g) * D;
   const uint16_t* vb = vc + (((size_t)b * ctx_max + t0) * n_kv + g) * D;
-  for (int i = tid; i < n * 16; i += kAttnThreads) {
+  const int n_cached = ROPE && t0 + n == L ? n - 1 : n;  // ROPE: the last row is the new token
+  for (int i = tid; i < n_cached * 16; i += kAttnThreads) {
     const int t = i >> 4, c = i & 15;
     *reinterpret_cast<uint4*>(Ks + t * kAttnRow + c * 8) = __ldg(reinterpret_cast<const uint4*>(kb + t * kv_stride + c * 8));
     *reinterpret_cast<uint4*>(Vs + t * kAttnRow + c * 8) = __ldg(reinterpret_cast<const uint4*>(vb + t * kv_stride + c * 8));
   }
-  for (int i = tid; i < G * D; i += kAttnThreads)
-    qs[i] = bf16_to_f32(q[(size_t)b * ld_q + (size_t)g * G * D + i]) * scale;
+  const uint16_t* qrow = q + (size_t)b * ld_q;
+  if (ROPE) {
+    const int p = L - 1;
+    constexpr int half = D / 2;
+    for (int i = tid; i < G * half; i += kAttnThreads) {  // (head, pair) -> two rotated q values
+      const int hh = i / half, j = i % half;
+      const float inv = powf(theta, -2.0f * (float)j / (float)D);
+      float sn, cs;
+      sincosf((float)p * inv, &sn, &cs);
+      const uint16_t* v = qrow + (size_t)(g * G + hh) * D;
+      const float x0 = bf16_to_f32(v[j]), x1 = bf16_to_f32(v[j + half]);
+      qs[hh * D + j] = __bfloat162float(__float2bfloat16_rn(x0 * cs - x1 * sn)) * scale;
+      qs[hh * D + j + half] = __bfloat162float(__float2bfloat16_rn(x1 * cs + x0 * sn)) * scale;
+    }
+    if (n_cached < n) {  // this split holds the new position: rotate k, stage + append k / v
+      const int t = n - 1, n_heads = G * n_kv;
+      const size_t cbase = (((size_t)b * ctx_max + p) * n_kv + g) * D;
+      if (tid < half) {
+        const int j = tid;
+        const float inv = powf(theta, -2.0f * (float)j / (float)D);
+        float sn, cs;
+        sincosf((float)p * inv, &sn, &cs);
+        const uint16_t* v = qrow + (size_t)(n_heads + g) * D;
+        const float x0 = bf16_to_f32(v[j]), x1 = bf16_to_f32(v[j + half]);
+        const uint16_t o0 = __bfloat16_as_ushort(__float2bfloat16_rn(x0 * cs - x1 * sn));
+        const uint16_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs + x0 * sn));
+        Ks[t * kAttnRow + j] = o0;
+        Ks[t * kAttnRow + j + half] = o1;
+        kc[cbase + j] = o0;
+        kc[cbase + j + half] = o1;
+      } else {
+        const int j = tid - half;
+        const uint16_t* vv = qrow + (size_t)(n_heads + n_kv + g) * D;
+        const uint16_t v0 = vv[j], v1 = vv[j + half];
+        Vs[t * kAttnRow + j] = v0;
+        Vs[t * kAttnRow + j + half] = v1;
+        vc[cbase + j] = v0;
+        vc[cbase + j + half] = v1;
+      }
+    }
+  } else {
+    for (int i = tid; i < G * D; i += kAttnThreads)
+      qs[i] = bf16_to_f32(qrow[(size_t)g * G * D + i]) * scale;
+  }
   __syncthreads();
   // scores: thread -> (head h, positions t, t + 32 ...) with 128 / G threads per head
   constexpr int TPH = kAttnThreads / G;
@@ -474,15 +524,15 @@ extern "C" uint64_t mesw_attention_workspace_bytes(int B, int n_heads, int ctx_m
   return (uint64_t)B * n_heads * S * kAttnPart * sizeof(float);
 }
 
-extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
-                                     const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
-                                     int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
-                                     int out_np, void* d_workspace, uint64_t workspace_bytes, float* d_corr,
-                                     int corr_ld, void* stream) {
+static int attention_decode(const uint16_t* d_q, int ld_q, uint16_t* d_kcache, uint16_t* d_vcache,
+                            const int32_t* d_len, int B, int n_heads, int n_kv, int head_dim, int ctx_max,
+                            uint16_t* d_out, int ld_out, int out_np, void* d_workspace, uint64_t workspace_bytes,
+                            float* d_corr, int corr_ld, bool rope, float theta, void* stream) {
   if (B <= 0 || n_kv <= 0 || n_heads % n_kv || ctx_max <= 0) return mesw_fail(MESW_ERR_VALUE, "attention: bad shape");
   if (head_dim != 128) return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: head_dim must be 128");
   if (!d_workspace || workspace_bytes < mesw_attention_workspace_bytes(B, n_heads, ctx_max))
     return mesw_fail(MESW_ERR_VALUE, "attention: workspace too small (mesw_attention_workspace_bytes)");
+  if (d_corr && corr_ld < n_heads) return mesw_fail(MESW_ERR_VALUE, "attention: corr_ld too small");
   const int G = n_heads / n_kv;
   const int S = (ctx_max + kAttnSplit - 1) / kAttnSplit;
   const float scale = 1.0f / sqrtf((float)head_dim);
@@ -490,20 +540,47 @@ extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16
   cudaStream_t s = (cudaStream_t)stream;
   float* part = reinterpret_cast<float*>(d_workspace);
   cudaError_t e;
+#define MESW_ATTN_CASE(GG)                                                                                     \
+  case GG:                                                                                                     \
+    e = rope ? mesw_launch(attn_partial_kernel<GG, true>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache,   \
+                           d_vcache, d_len, n_kv, ctx_max, scale, part, S, theta)                              \
+             : mesw_launch(attn_partial_kernel<GG, false>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache,  \
+                           d_vcache, d_len, n_kv, ctx_max, scale, part, S, theta);                             \
+    break;
   switch (G) {
-    case 1: e = mesw_launch(attn_partial_kernel<1>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
-    case 2: e = mesw_launch(attn_partial_kernel<2>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
-    case 4: e = mesw_launch(attn_partial_kernel<4>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
-    case 8: e = mesw_launch(attn_partial_kernel<8>, grid, dim3(kAttnThreads), 0, s, d_q, ld_q, d_kcache, d_vcache, d_len, n_kv, ctx_max, scale, part, S); break;
+    MESW_ATTN_CASE(1)
+    MESW_ATTN_CASE(2)
+    MESW_ATTN_CASE(4)
+    MESW_ATTN_CASE(8)
     default:
       return mesw_fail(MESW_ERR_UNSUPPORTED, "attention: heads per kv head must be 1, 2, 4 or 8");
   }
+#undef MESW_ATTN_CASE
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
-  if (d_corr && corr_ld < n_heads) return mesw_fail(MESW_ERR_VALUE, "attention: corr_ld too small");
   e = mesw_launch(attn_merge_kernel, dim3(B, n_heads), dim3(128), 0, s, (const float*)part, d_len, n_heads, S, d_out,
                   ld_out, out_np, d_corr, corr_ld);
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("attention_decode");
+}
+
+extern "C" int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,
+                                     const uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
+                                     int n_kv, int head_dim, int ctx_max, uint16_t* d_out, int ld_out,
+                                     int out_np, void* d_workspace, uint64_t workspace_bytes, float* d_corr,
+                                     int corr_ld, void* stream) {
+  // read-only caches (the non-ROPE instance never writes them)
+  return attention_decode(d_q, ld_q, const_cast<uint16_t*>(d_kcache), const_cast<uint16_t*>(d_vcache), d_len, B,
+                          n_heads, n_kv, head_dim, ctx_max, d_out, ld_out, out_np, d_workspace, workspace_bytes,
+                          d_corr, corr_ld, false, 0.f, stream);
+}
+
+extern "C" int mesw_attention_decode_rope(const uint16_t* d_qkv, int ld_qkv, uint16_t* d_kcache,
+                                          uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads, int n_kv,
+                                          int head_dim, float theta, int ctx_max, uint16_t* d_out, int ld_out,
+                                          int out_np, void* d_workspace, uint64_t workspace_bytes, float* d_corr,
+                                          int corr_ld, void* stream) {
+  return attention_decode(d_qkv, ld_qkv, d_kcache, d_vcache, d_len, B, n_heads, n_kv, head_dim, ctx_max, d_out,
+                          ld_out, out_np, d_workspace, workspace_bytes, d_corr, corr_ld, true, theta, stream);
 }
 
 extern "C" int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, int ld_out,

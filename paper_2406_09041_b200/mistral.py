@@ -14,6 +14,7 @@ libmesw.so) is captured once in a CUDA graph and replayed.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,6 +24,9 @@ from . import _lib
 from .device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan, _stream,
                      Workspace, canonical_numel, canonical_rows, corr_table, cta_candidates, tune_num_ctas)
 from .synth import MistralShape
+
+# rope + KV-cache append run inside the attention launch (mesw_attention_decode_rope)
+_FUSED_ROPE = os.environ.get("MESW_ROPE_SPLIT") is None
 
 PROJ_ORDER = ("q", "k", "v", "o", "gate", "up", "down")
 
@@ -332,15 +336,23 @@ class MistralMultiExpert:
                                    bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "xn"), st))
                 layers[l][0](stream)
             kc, vc = self.kcache[l], self.vcache[l]
-            chk(L.mesw_rope_append(self.qkv.data_ptr(), self.qkv.stride(0), self.pos.data_ptr(), B, s.n_heads,
-                                   s.n_kv_heads, s.head_dim, C.c_float(s.rope_theta), kc.data_ptr(),
-                                   vc.data_ptr(), self.ctx_max, st))
+            if not _FUSED_ROPE:  # two-call form (A/B switch MESW_ROPE_SPLIT=1)
+                chk(L.mesw_rope_append(self.qkv.data_ptr(), self.qkv.stride(0), self.pos.data_ptr(), B, s.n_heads,
+                                       s.n_kv_heads, s.head_dim, C.c_float(s.rope_theta), kc.data_ptr(),
+                                       vc.data_ptr(), self.ctx_max, st))
             for (r0, r1, bufs, layers, _) in self._plans:
-                chk(L.mesw_attention_decode(rows_ptr(self.qkv, r0), self.qkv.stride(0), rows_ptr(kc, r0),
-                                            rows_ptr(vc, r0), self.len.data_ptr() + 4 * r0, r1 - r0, s.n_heads,
-                                            s.n_kv_heads, s.head_dim, self.ctx_max, bufs["attn"].data_ptr(), 0,
-                                            canonical_rows(r1 - r0), self.attn_ws.data_ptr(), self.attn_ws.numel(),
-                                            *corr(bufs, "attn"), st))
+                if _FUSED_ROPE:  # rope + KV append folded into the attention launch (len = pos + 1)
+                    chk(L.mesw_attention_decode_rope(
+                        rows_ptr(self.qkv, r0), self.qkv.stride(0), rows_ptr(kc, r0), rows_ptr(vc, r0),
+                        self.len.data_ptr() + 4 * r0, r1 - r0, s.n_heads, s.n_kv_heads, s.head_dim,
+                        C.c_float(s.rope_theta), self.ctx_max, bufs["attn"].data_ptr(), 0, canonical_rows(r1 - r0),
+                        self.attn_ws.data_ptr(), self.attn_ws.numel(), *corr(bufs, "attn"), st))
+                else:
+                    chk(L.mesw_attention_decode(rows_ptr(self.qkv, r0), self.qkv.stride(0), rows_ptr(kc, r0),
+                                                rows_ptr(vc, r0), self.len.data_ptr() + 4 * r0, r1 - r0, s.n_heads,
+                                                s.n_kv_heads, s.head_dim, self.ctx_max, bufs["attn"].data_ptr(), 0,
+                                                canonical_rows(r1 - r0), self.attn_ws.data_ptr(),
+                                                self.attn_ws.numel(), *corr(bufs, "attn"), st))
                 layers[l][1](stream)
             for (r0, r1, bufs, layers, _) in self._plans:
                 chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), lw.mlp_norm.data_ptr(), r1 - r0, H, eps,
@@ -360,7 +372,8 @@ class MistralMultiExpert:
 
     def launches_per_step(self) -> int:
         g = len(self.groups)
-        return 1 + (1 + g * 9) * self.n_layers + g * 2 + 2  # attention is 2 kernels
+        per_layer = g * 9 + (0 if _FUSED_ROPE else 1)  # attention is 2 kernels (rope folded in)
+        return 1 + per_layer * self.n_layers + g * 2 + 2
 
     def capture(self) -> None:
         """Capture one decode step in a CUDA graph (replayed by `replay`)."""
