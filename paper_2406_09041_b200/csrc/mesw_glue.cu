@@ -91,11 +91,17 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
                                                                uint16_t* __restrict__ y, int ldy, int ynp,
                                                                float* __restrict__ corr, int corr_ld) {
   pdl_trigger();
-  pdl_wait();  // inputs may come from the previous kernel in the stream
   __shared__ float red[32];
   const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)blockIdx.x * ldx);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   const int nvec = H / 8;
+  uint4 gw[kNormMaxVec];  // the norm weights are static: read them while the producer drains
+#pragma unroll
+  for (int j = 0; j < kNormMaxVec; ++j) {
+    const int i = threadIdx.x + j * kNormThreads;
+    if (i < nvec) gw[j] = __ldg(wr + i);
+  }
+  pdl_wait();  // x comes from the previous kernel in the stream
   uint4 v[kNormMaxVec];
   float ss = 0.f;
 #pragma unroll
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* _
     const int i = threadIdx.x + j * kNormThreads;
     float c = 0.f;
     if (i < nvec) {
-      const uint4 g4 = wr[i];
+      const uint4 g4 = gw[j];
       const uint32_t* e = reinterpret_cast<const uint32_t*>(&v[j]);
       const uint32_t* g = reinterpret_cast<const uint32_t*>(&g4);
       uint4 o;
