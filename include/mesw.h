@@ -224,7 +224,7 @@ int mesw_rope_append(uint16_t* d_qkv, int ld_qkv, const int32_t* d_pos, int B, i
                      int n_kv, int head_dim, float theta, uint16_t* d_kcache,
                      uint16_t* d_vcache, int ctx_max, void* stream);
 /* GQA decode attention over len[b] cached positions; out [B][n_heads*head_dim].
- * Split over the context in 64-position blocks (partials in `workspace`, then merged);
+ * Split over the context in 32-position blocks (partials in `workspace`, then merged);
  * workspace >= mesw_attention_workspace_bytes(B, n_heads, ctx_max). head_dim 128. */
 uint64_t mesw_attention_workspace_bytes(int B, int n_heads, int ctx_max);
 int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcache,

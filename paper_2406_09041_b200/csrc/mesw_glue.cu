@@ -183,12 +183,15 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int ld_qkv, const
 //   softmax: block reductions per head (fixed order),
 //   P.V: thread = (4-dim group, position slice), slices reduced through smem.
 // GQA decode attention, split over the context (flash-decoding): CTA (b, kv head g, split s)
-// handles positions [64 s, 64 s + 64) for the G query heads of kv head g and writes a
+// handles positions [P s, P s + P) (P = kAttnSplit) for the G query heads of kv head g and writes a
 // partial (running max, sum of exponentials, unnormalised output) per head; a second
 // kernel merges the splits.  Many small CTAs stream the KV cache at full occupancy
 // (the cache is read once per step: an HBM-bound pass).  D must be 128.
 constexpr int kAttnThreads = 128;
-constexpr int kAttnSplit = 64;     // positions per CTA
+#ifndef MESW_ATTN_SPLIT
+#define MESW_ATTN_SPLIT 32  // measured on C2 (B=32, ctx 129-256): 32 > 64 (+0.5-1 %) > 16
+#endif
+constexpr int kAttnSplit = MESW_ATTN_SPLIT;  // positions per CTA
 constexpr int kAttnRow = 136;      // bf16 per staged row (128 + 8 pad: conflict-free row reads)
 constexpr int kAttnPart = 2 + 128; // floats per (b, head, split) partial: m, l, o[128]
 
