@@ -403,10 +403,23 @@ __global__ void argmax_kernel(const void* __restrict__ logits, int is_bf16, int 
   const int b = blockIdx.x;
   float best = -INFINITY;
   int bidx = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float v = is_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(logits)[(size_t)b * ld + i])
-                            : reinterpret_cast<const float*>(logits)[(size_t)b * ld + i];
-    if (bidx == 0x7fffffff || v > best) { best = v; bidx = i; }  // i ascending: ties keep the first
+  if (is_bf16 && V % 8 == 0 && ld % 8 == 0) {  // 16-byte loads: 8 logits per thread per pass
+    const uint4* row = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(logits) + (size_t)b * ld);
+    for (int c = threadIdx.x; c < V / 8; c += blockDim.x) {
+      const uint4 q = __ldg(row + c);
+      const uint32_t* e = reinterpret_cast<const uint32_t*>(&q);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // ascending index inside the chunk: ties keep the first
+        const float v = (k & 1) ? bf16_hi(e[k >> 1]) : bf16_lo(e[k >> 1]);
+        if (bidx == 0x7fffffff || v > best) { best = v; bidx = 8 * c + k; }
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      const float v = is_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(logits)[(size_t)b * ld + i])
+                              : reinterpret_cast<const float*>(logits)[(size_t)b * ld + i];
+      if (bidx == 0x7fffffff || v > best) { best = v; bidx = i; }  // i ascending: ties keep the first
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -89,3 +89,23 @@ def test_attention_decode_rope_matches_two_call_form(lens, G, ctx_max):
         assert torch.equal(outs[1][3][b, :n - 1], vc0[b, :n - 1])
         assert torch.equal(outs[1][3][b, n:], vc0[b, n:])
         assert not torch.equal(outs[1][2][b, n - 1], kc0[b, n - 1])
+
+
+@pytest.mark.parametrize("V,is_bf16", [(32000, 1), (32003, 1), (1000, 0), (8, 1)])
+def test_argmax_first_max(V, is_bf16):
+    """mesw_argmax == np.argmax (ties -> lowest id, toylm.py:247) on the vectorised bf16 path,
+    the scalar fallback (V % 8 != 0) and f32 logits; rows with planted ties."""
+    import torch
+    from paper_2406_09041_b200 import _lib
+    L = _lib.lib()
+    B = 5
+    rng = np.random.default_rng(V)
+    x = rng.integers(-40, 40, size=(B, V)).astype(np.float32) / 8  # exact in bf16, many ties
+    x[1, :] = 0.0
+    x[2, V // 3] = x[2, V - 1] = 100.0
+    dt = torch.bfloat16 if is_bf16 else torch.float32
+    t = torch.from_numpy(x).to(dt).cuda()
+    out = torch.full((B,), -1, dtype=torch.int32, device="cuda")
+    _lib.check(L.mesw_argmax(t.data_ptr(), is_bf16, B, V, t.stride(0), out.data_ptr(),
+                             C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    assert out.cpu().numpy().tolist() == np.argmax(t.float().cpu().numpy(), axis=1).tolist()
