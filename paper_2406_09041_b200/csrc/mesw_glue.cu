@@ -84,8 +84,11 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __
 
 // y = x * rsqrt(mean(x^2) + eps) * w   (one CTA per token; row held in registers,
 // one 16-byte load per 8 elements, single global pass)
-constexpr int kNormThreads = 256;
-constexpr int kNormMaxVec = 4;  // up to 256 * 4 * 8 = 8192 channels
+#ifndef MESW_NORM_THREADS
+#define MESW_NORM_THREADS 256
+#endif
+constexpr int kNormThreads = MESW_NORM_THREADS;
+constexpr int kNormMaxVec = 2048 / MESW_NORM_THREADS;  // up to 8192 channels
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* __restrict__ x, int ldx,
                                                                const uint16_t* __restrict__ w, int H, float eps,
                                                                uint16_t* __restrict__ y, int ldy, int ynp,
