@@ -40,6 +40,7 @@ def build_engine(B, E, seed=0, n_layers=None, device="cuda", experts=None, reque
     shape = synth.MistralShape()
     eng = MistralMultiExpert(shape, max_batch=B + 16 * len(experts), ctx_max=CTX, device=device,
                              n_layers=n_layers)
+    eng.wrap_positions = True  # steady-state benchmark: long runs wrap positions (never in serving)
     eng.load_synthetic_base(seed=seed)
     shapes = synth.mistral_expert_shapes(shape, eng.n_layers)
     names = _expert_names(max(experts) + 1)

@@ -46,7 +46,8 @@ typedef enum {
   MESW_ERR_TRUNCATED = 3,           /* errors.TruncatedArtifactError (errors.py:31) */
   MESW_ERR_VALUE = 4,               /* ValueError (shape / range / bits)            */
   MESW_ERR_CUDA = 5,                /* CUDA runtime failure                          */
-  MESW_ERR_UNSUPPORTED = 6          /* valid input this build does not handle        */
+  MESW_ERR_UNSUPPORTED = 6,         /* valid input this build does not handle        */
+  MESW_ERR_INDEX = 7                /* IndexError (salient index >= input channels)  */
 } mesw_status;
 
 #define MESW_TILE_N 128 /* outputs per column group  */
@@ -115,8 +116,10 @@ int mesw_repack_weight(const uint16_t* d_src, uint32_t m, uint32_t n, uint32_t l
 /* Host helper: build the per-column-group salient tables of a fused linear from
  * its blocks.  Block b covers output columns [col_base[b], col_base[b]+n[b]),
  * has k[b] salient input channels h_idx[b][...] and rows h_rows[b] (k x n
- * binary16).  Call once with the out pointers NULL to get *total, then again.  */
-int mesw_build_salient_tables(uint32_t n_blocks, const uint32_t* col_base, const uint32_t* n,
+ * binary16).  Call once with the out pointers NULL to get *total, then again.
+ * Indices must be strictly ascending and < m (input channels); otherwise
+ * MESW_ERR_INDEX (the reference's reconstruct() raises IndexError, compress.py:119-120). */
+int mesw_build_salient_tables(uint32_t m, uint32_t n_blocks, const uint32_t* col_base, const uint32_t* n,
                               const uint32_t* k, const uint32_t* const* h_idx,
                               const uint16_t* const* h_rows, uint32_t n_total_pad,
                               int32_t* h_sal_off, int32_t* h_sal_idx, uint16_t* h_sal_rows,
@@ -248,7 +251,9 @@ int mesw_swiglu(const uint16_t* d_gu, int ld_gu, int B, int I, uint16_t* d_out, 
 /* Greedy next token: argmax with ties to the lowest id (toylm.py:247). */
 int mesw_argmax(const void* d_logits, int is_bf16, int B, int V, int ld, int32_t* d_out,
                 void* stream);
-/* Decode bookkeeping: pos[b] += 1 (wrapping to wrap_to at ctx_max), len[b] = pos[b] + 1. */
+/* Decode bookkeeping: pos[b] += 1, len[b] = pos[b] + 1.  wrap_to >= 0 wraps a request that
+ * reaches ctx_max back to wrap_to (benchmark steady state); wrap_to < 0 never wraps (serving:
+ * the host checks the cache window before each step). */
 int mesw_advance_positions(int32_t* d_pos, int32_t* d_len, int B, int ctx_max, int wrap_to,
                            void* stream);
 
@@ -297,7 +302,7 @@ int mesw_quantize_pack(const float* d_delta, uint32_t m, uint32_t n, const float
  * hashing and f64 summation order as pinned in oracle/router.py.
  *   d_codepoints  int32 Unicode code points of all queries, concatenated
  *   d_offsets     int64[B+1]: query q = code points [off[q], off[q+1])
- *   d_loglik      f32[D][65536], d_logprior f32[D], 1 <= D <= 6
+ *   d_loglik      f32[D][65536], d_logprior f32[D], 1 <= D <= 32 (one warp lane per domain)
  * Outputs: d_domain[B] (argmax, ties -> lowest id), d_conf[B] (softmax of the
  * winner), d_prior_only[B] (1 when the query has no n-gram; may be NULL).      */
 int mesw_router_classify(const int32_t* d_codepoints, const int64_t* d_offsets, int B,

@@ -71,6 +71,39 @@ def unpack_codes(data: bytes, rows: int, cols: int, bits: int) -> np.ndarray:
     if rows == 0 or cols == 0:
         return np.zeros((rows, cols), dtype=np.int8)
     bpc = bytes_per_col(rows, bits)
+    if bits == 2:  # byte-aligned fields: 4 codes per byte, LSB first (same result, vectorised)
+        run = np.frombuffer(data, dtype=np.uint8).reshape(cols, bpc)
+        u = np.empty((cols, bpc, 4), dtype=np.int8)
+        for f in range(4):
+            u[:, :, f] = (run >> np.uint8(2 * f)) & np.uint8(3)
+        q = u.reshape(cols, 4 * bpc)[:, :rows] - np.int8(q_n)
+        return np.ascontiguousarray(q.T)
+    runs = np.zeros((cols, bpc + 1), dtype=np.uint16)
+    runs[:, :bpc] = np.frombuffer(data, dtype=np.uint8).reshape(cols, bpc)
+    bit_off = np.arange(rows, dtype=np.int64) * bits
+    lo = bit_off >> 3
+    sh = (bit_off & 7).astype(np.uint16)
+    window = runs[:, lo] | (runs[:, lo + 1] << np.uint16(8))  # [cols, rows]
+    u = ((window >> sh[None, :]) & np.uint16((1 << bits) - 1)).astype(np.int16)
+    q = (2 * u - 1) if bits == 1 else (u - q_n)
+    return np.ascontiguousarray(q.T.astype(np.int8))
+
+
+def _unpack_window(data: bytes, rows: int, cols: int, bits: int) -> np.ndarray:
+    """Decode a column-major LSB-first offset-code stream to int8 codes [rows, cols].
+
+    Follows quant.py:216-236: column j owns bytes [j*bpc, (j+1)*bpc); row i's
+    offset occupies bits [i*b, i*b+b) of that run, little-endian bit order;
+    q = u - Q_N for b>=2 and q = 2u - 1 for b=1.  Implemented with a two-byte
+    window per value (a b<=8 value spans at most two bytes).
+    """
+    expected = packed_nbytes(rows, cols, bits)
+    if len(data) != expected:
+        raise ValueError(f"packed stream has {len(data)} bytes, expected {expected}")
+    q_n, _ = code_range(bits)
+    if rows == 0 or cols == 0:
+        return np.zeros((rows, cols), dtype=np.int8)
+    bpc = bytes_per_col(rows, bits)
     runs = np.zeros((cols, bpc + 1), dtype=np.uint16)
     runs[:, :bpc] = np.frombuffer(data, dtype=np.uint8).reshape(cols, bpc)
     bit_off = np.arange(rows, dtype=np.int64) * bits
@@ -127,6 +160,10 @@ class OracleLayer:
 
     def codes(self) -> np.ndarray:
         return unpack_codes(self.packed, self.m, self.n, self.bits)
+
+    def unpack_generic(self) -> np.ndarray:
+        """The two-byte-window decode for every width (pins the vectorised 2-bit path)."""
+        return _unpack_window(self.packed, self.m, self.n, self.bits)
 
     def reconstruct(self) -> np.ndarray:
         """Dense f32 delta: codes*steps, salient rows overwritten (compress.py:115-121)."""

@@ -29,7 +29,7 @@ import numpy as np
 N_BUCKETS = 1 << 16
 FNV_OFFSET = 2166136261
 FNV_PRIME = 16777619
-MAX_DOMAINS = 6  # the paper's template enumerates A..F
+MAX_DOMAINS = 32  # one warp lane per domain in K4; render_prompt alone caps at 6
 
 
 def fnv1a32(data: bytes) -> int:
@@ -60,7 +60,7 @@ def train_router(records, domains) -> OracleRouter:
     """records: iterable of (query, domain name).  SPEC.md:540-545."""
     domains = tuple(domains)
     if not domains or len(domains) > MAX_DOMAINS:
-        raise ValueError("1..6 domains")
+        raise ValueError(f"1..{MAX_DOMAINS} domains")
     index = {d: i for i, d in enumerate(domains)}
     counts = np.zeros((len(domains), N_BUCKETS), dtype=np.int64)
     ndoc = np.zeros(len(domains), dtype=np.int64)

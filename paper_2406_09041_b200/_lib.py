@@ -57,7 +57,7 @@ _SIGNATURES = [
                                     C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]),
     ("mesw_repack_weight", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p,
                                      C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]),
-    ("mesw_build_salient_tables", C.c_int, [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+    ("mesw_build_salient_tables", C.c_int, [C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.POINTER(C.c_uint64)]),
     ("mesw_unpack_codes_debug", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -130,6 +130,7 @@ _STATUS_EXC = {
     4: ValueError,
     5: RuntimeError,
     6: NotImplementedError,
+    7: IndexError,
 }
 
 

@@ -169,7 +169,7 @@ extern "C" int mesw_parse_layers(const uint8_t* h_buf, uint64_t len, uint64_t fi
   return MESW_OK;
 }
 
-extern "C" int mesw_build_salient_tables(uint32_t n_blocks, const uint32_t* col_base,
+extern "C" int mesw_build_salient_tables(uint32_t m, uint32_t n_blocks, const uint32_t* col_base,
                                          const uint32_t* n, const uint32_t* k,
                                          const uint32_t* const* h_idx,
                                          const uint16_t* const* h_rows, uint32_t n_total_pad,
@@ -177,6 +177,12 @@ extern "C" int mesw_build_salient_tables(uint32_t n_blocks, const uint32_t* col_
                                          uint16_t* h_sal_rows, uint64_t* total) {
   if (n_total_pad % MESW_TILE_N) return mesw_fail(MESW_ERR_VALUE, "n_total_pad % 128 != 0");
   const uint32_t n_cg = n_total_pad / MESW_TILE_N;
+  for (uint32_t b = 0; b < n_blocks; ++b)
+    for (uint32_t r = 0; r < k[b]; ++r) {
+      // an out-of-range index would make the fused kernel read x outside the row
+      if (h_idx[b][r] >= m) return mesw_fail(MESW_ERR_INDEX, "salient index out of range");
+      if (r && h_idx[b][r] <= h_idx[b][r - 1]) return mesw_fail(MESW_ERR_VALUE, "salient indices must ascend");
+    }
   uint64_t acc = 0;
   for (uint32_t cg = 0; cg < n_cg; ++cg) {
     const uint64_t c0 = (uint64_t)cg * MESW_TILE_N;

@@ -492,8 +492,9 @@ __global__ void unpack_x_kernel(const uint16_t* __restrict__ xc, int B, int m, i
   y[(size_t)t * ldy + k] = xc[canon_index(t, k, NP)];
 }
 
-// Advance every request by one position (pos += 1, len = pos + 1); a request that
-// reaches the end of its cache window wraps back to `wrap_to` (bench steady state).
+// Advance every request by one position (pos += 1, len = pos + 1).  wrap_to >= 0: a request
+// that reaches the end of its cache window wraps back to `wrap_to` (bench steady state only);
+// wrap_to < 0 (serving): no wrap -- the host refuses a step that would pass the window.
 __global__ void advance_kernel(int32_t* __restrict__ pos, int32_t* __restrict__ len, int B, int ctx_max,
                                int wrap_to) {
   pdl_trigger();
@@ -501,7 +502,7 @@ __global__ void advance_kernel(int32_t* __restrict__ pos, int32_t* __restrict__ 
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int p = pos[b] + 1;
-  if (p >= ctx_max) p = wrap_to;
+  if (p >= ctx_max && wrap_to >= 0) p = wrap_to;
   pos[b] = p;
   len[b] = p + 1;
 }
@@ -512,7 +513,7 @@ using namespace mesw;
 
 extern "C" int mesw_advance_positions(int32_t* d_pos, int32_t* d_len, int B, int ctx_max, int wrap_to,
                                       void* stream) {
-  if (B <= 0 || wrap_to < 0 || wrap_to >= ctx_max) return mesw_fail(MESW_ERR_VALUE, "advance: bad args");
+  if (B <= 0 || wrap_to >= ctx_max) return mesw_fail(MESW_ERR_VALUE, "advance: bad args");
   mesw_launch(advance_kernel, dim3((B + 127) / 128), dim3(128), 0, (cudaStream_t)stream, d_pos, d_len, B, ctx_max, wrap_to);
   return mesw_check_launch("advance_positions");
 }

@@ -101,7 +101,8 @@ struct LinearParams {
   int ring_bytes;  // dynamic shared memory past the Smem header
   const float* x_corr;  // offset-code bias table [t * x_corr_ld + ks] (OFF kernels)
   int x_corr_ld;
-  int n_iss;  // MMA issuer threads (a tcgen05.mma stream runs ~60-85 cycles/instr per issuer)
+  int n_iss;  // MMA issuer warps (a tcgen05.mma stream runs ~40 cycles/instr per issuer)
+  int n_dq;   // delta issuers = active dequant groups (group g feeds delta issuer g)
   unsigned long long* tbuf;  // MESW_TIMING: per-CTA globaltimer stamps
   int dbg;  // reserved (MESW_DBG)
 };
@@ -186,6 +187,38 @@ __device__ __forceinline__ void mma2_ts_w(uint32_t d, uint32_t a_tmem, uint64_t 
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
+// One whole k-step (K = 128 = 8 x 16) of a cta_group::2 MMA chain in ONE asm block with one
+// elect: the descriptor / TMEM-address increments are immediates inside the block, so ptxas
+// keeps them in the uniform datapath (no per-instruction R2UR.BROADCAST round trip, which
+// made every tcgen05.mma cost ~40 cycles of issue).  Callers pass warp-uniform operands
+// (uni()): then the operands themselves need no broadcast either.
+__device__ __forceinline__ uint32_t uni(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+__device__ __forceinline__ uint64_t uni64(uint64_t v) {
+  return ((uint64_t)uni((uint32_t)(v >> 32)) << 32) | uni((uint32_t)v);
+}
+#define MESW_SS_STEP(J)                                                   \
+  "add.s64 ad, %1, " #J "*16;\nadd.s64 bd, %2, " #J "*16;\n"              \
+  "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ad, bd, %3, 1;\n"
+__device__ __forceinline__ void mma2_ss_k128(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b64 ad, bd;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      MESW_SS_STEP(1) MESW_SS_STEP(2) MESW_SS_STEP(3) MESW_SS_STEP(4) MESW_SS_STEP(5) MESW_SS_STEP(6)
+      MESW_SS_STEP(7) "}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+#undef MESW_SS_STEP
+#define MESW_TS_STEP(J)                                                   \
+  "add.u32 at, %1, " #J "*8;\nadd.s64 bd, %2, " #J "*16;\n"               \
+  "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [at], bd, %3, 1;\n"
+__device__ __forceinline__ void mma2_ts_k128(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b32 at;\n.reg .b64 bd;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      MESW_TS_STEP(1) MESW_TS_STEP(2) MESW_TS_STEP(3) MESW_TS_STEP(4) MESW_TS_STEP(5) MESW_TS_STEP(6)
+      MESW_TS_STEP(7) "}\n" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+#undef MESW_TS_STEP
+
 __device__ __forceinline__ void tc2_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -612,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     const uint32_t peer_relay = rank == 0 ? 2 : 1;  // leader: own tile + peer relay
     for (int i = 0; i < p.nx; ++i) { mbar_init(&S.xfull[i], peer_relay); mbar_init(&S.xempty[i], p.n_iss); }
     for (int i = 0; i < p.nw; ++i) { mbar_init(&S.wfull[i], peer_relay); mbar_init(&S.wempty[i], 1); }
-    for (int i = 0; i < p.nc; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 128 * kDqGroups); }
+    for (int i = 0; i < p.nc; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 128 * p.n_dq); }
     for (int i = 0; i < p.n_aslots; ++i) { mbar_init(&S.afull[i], 8); mbar_init(&S.aempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&S.accfull[i], p.n_iss); mbar_init(&S.accempty[i], 8); }
     mbar_init(&S.finbar, 1);
@@ -784,9 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             MESW_PROF(tq = clock64();)
             tc_fence_after();
             const uint64_t wd = wdesc0 + (uint64_t)(sw * wstride);
-            mma2_ss_w(d_base, wd, xd, id_base, f0);
-#pragma unroll
-            for (int j = 1; j < 8; ++j) mma2_ss_w(d_base, wd + 16 * j, xd + 16 * j, id_base, 1u);
+            mma2_ss_k128(uni(d_base), uni64(wd), uni64(xd), uni(id_base), uni(f0));
             tc2_commit_w(&S.wempty[sw]);
             if (++sw == p.nw) { sw = 0; pw ^= 1; }
             MESW_PROF(prof[2] += clock64() - tq;)
@@ -807,9 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
               const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
 #ifndef MESW_EXP_NOMMA
-              mma2_ts_w(dd, a0, bd, id, f0);
-#pragma unroll
-              for (int j = 1; j < 8; ++j) mma2_ts_w(dd, a0 + 8 * j, bd + 16 * j, id, 1u);
+              mma2_ts_k128(uni(dd), uni(a0), uni64(bd), uni(id), uni(f0));
 #endif
               tc2_commit_w(&S.aempty[abase_own + aslot]);
               if (++aslot == na_own) { aslot = 0; aph ^= 1; }
@@ -836,103 +865,87 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     }
   } else if (warp < kEpiWarp0) {
     // ===================== dequant groups: own codes -> own TMEM A rows =====================
+    // Issuer-affine groups: group g serves delta issuer g (segments q = g, g + n_dq, ...) and
+    // walks that issuer's A sub-ring with two registers (position, laps).  No per-job issuer
+    // lookup, no skipped jobs, no data-dependent branches in the loop: the profile of the
+    // previous slot-affine form showed the dequant warps ~80 % busy on that bookkeeping
+    // (branch_resolving / dependent-latency stalls), not on the expansion or the TMEM stores.
     const int grp = (warp - kDqWarp0) >> 2;
     const int quarter = warp & 3;
     const int mrow = quarter * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     constexpr int WPK = CHB / 4;  // code words per k-half of a channel
-    int sc = 0;
-    uint32_t pc = 0;
-    // per issuer: position in its A sub-ring and completed laps (no divisions in the loop)
-    int ps0 = 0, ps1 = 0, ps2 = 0, us0 = 0, us1 = 0, us2 = 0;
-    const int na0 = p.a_na[0], na1 = p.a_na[1], na2 = p.a_na[2];
-    const int ab0 = p.a_base[0], ab1 = p.a_base[1], ab2 = p.a_base[2];
-    const int iss_first = (has_w && p.n_iss > 1) ? 1 : 0, iss_last = p.n_iss - 1;
+    const int n_dq = p.n_dq;
     MESW_PROF(long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
     MESW_PROF(const long long dstart = clock64();)
     MESW_PROF(int dcount = 0;)
     MESW_PROF(long long dq;)
-    for (int pi = 0; pi < (p.n_seg > 0 ? po.np : 0); ++pi) {
-      long long pa, pb;
-      po.bounds(pi, pa, pb);
-      for (long long u = pa; u < pb; ++u) {
-        int q_iss = iss_first;  // issuer of segment 0
-        for (int ch = 0; ch < p.n_chunks; ++ch) {
-          const int sg0 = ch * p.segs_per_chunk;
-          const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
-          MESW_PROF(dq = clock64();)
-          mbar_wait(&S.cfull[sc], pc);
-          MESW_PROF(dprof[0] += clock64() - dq;)
-          const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
-          for (int q = sg0; q < sg1; ++q) {
-            const int iss = q_iss;  // == seg_issuer(q): register-only bookkeeping (no smem / indexed loads)
-            q_iss = q_iss == iss_last ? iss_first : q_iss + 1;
-            const int pos = iss == 0 ? ps0 : (iss == 1 ? ps1 : ps2);
-            const int use = iss == 0 ? us0 : (iss == 1 ? us1 : us2);
-            const int na_i = iss == 0 ? na0 : (iss == 1 ? na1 : na2);
-            const int ab_i = iss == 0 ? ab0 : (iss == 1 ? ab1 : ab2);
-            {
-              const bool wrap = pos + 1 == na_i;
-              const int np1 = wrap ? 0 : pos + 1, nu = use + (wrap ? 1 : 0);
-              if (iss == 0) { ps0 = np1; us0 = nu; } else if (iss == 1) { ps1 = np1; us1 = nu; } else { ps2 = np1; us2 = nu; }
-            }
-            // slot-affine groups: A slot s is always filled by group s % 2 (whole jobs, both
-            // k-halves: two independent dequant chains per thread), so every slot is written
-            // by one group and read by one issuer, in sequence
-            const int aslot = ab_i + pos;
-            if (aslot % kDqGroups != grp) continue;
-            uint32_t cw[2 * WPK];
-            const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
-#pragma unroll
-            for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-              for (int v = 0; v < CHB / 16; ++v) {
-                const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
-                const int w0 = kh * WPK + 4 * v;
-                cw[w0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
-              }
-            MESW_PROF(const bool jst = p.tbuf && blockIdx.x == 0 && threadIdx.x == kDqWarp0 * 32 + grp * 128 && dprof[7] < 32;)
-            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7]] = clock64();)
+    if (grp < n_dq) {
+      const int irole = grp + ((has_w && p.n_iss > 1) ? 1 : 0);  // the issuer warp this group feeds
+      const int na = p.a_na[irole], ab = p.a_base[irole];
+      int pos = 0, use = 0;
+      int sc = 0;
+      uint32_t pc = 0;
+      for (int pi = 0; pi < po.np; ++pi) {
+        long long pa, pb;
+        po.bounds(pi, pa, pb);
+        for (long long u = pa; u < pb; ++u) {
+          for (int ch = 0; ch < p.n_chunks; ++ch) {
+            const int sg0 = ch * p.segs_per_chunk;
+            const int sg1 = min(p.n_seg, sg0 + p.segs_per_chunk);
             MESW_PROF(dq = clock64();)
-            if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
-            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 1] = clock64();)
-            MESW_PROF(dprof[1] += clock64() - dq;)
-            MESW_PROF(dq = clock64();)
-            const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
+            mbar_wait(&S.cfull[sc], pc);
+            MESW_PROF(dprof[0] += clock64() - dq;)
+            const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
+            for (int q = sg0 + ((grp - sg0 % n_dq) + n_dq) % n_dq; q < sg1; q += n_dq) {
+              const int aslot = ab + pos;
+              uint32_t cw[2 * WPK];
+              const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
+#pragma unroll
+              for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+                for (int v = 0; v < CHB / 16; ++v) {
+                  const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
+                  const int w0 = kh * WPK + 4 * v;
+                  cw[w0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
+                }
+              MESW_PROF(const bool jst = p.tbuf && blockIdx.x == 0 && threadIdx.x == kDqWarp0 * 32 + grp * 128 && dprof[7] < 32;)
+              MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7]] = clock64();)
+              MESW_PROF(dq = clock64();)
+              if (use > 0) mbar_wait(&S.aempty[aslot], (uint32_t)((use - 1) & 1));
+              MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 1] = clock64();)
+              MESW_PROF(dprof[1] += clock64() - dq;)
+              MESW_PROF(dq = clock64();)
+              const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
 #ifndef MESW_EXP_NODQ
 #pragma unroll
-            for (int kh = 0; kh < MESW_EXP_KH; ++kh) {
-              uint32_t r[32];
-              if (OFF) dequant_chunk2_offset(&cw[kh * WPK], r);
-              else dequant_chunk<DB>(&cw[kh * WPK], r);
-#ifdef MESW_EXP_ST1  // experiment: expand both halves, store only the first (TMEM-store cost probe)
-              if (kh == 1) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) asm volatile("" ::"r"(r[i]));
-                continue;
+              for (int kh = 0; kh < MESW_EXP_KH; ++kh) {
+                uint32_t r[32];
+                if (OFF) dequant_chunk2_offset(&cw[kh * WPK], r);
+                else dequant_chunk<DB>(&cw[kh * WPK], r);
+                tmem_st32(a0 + lane_addr + 32 * kh, r);
               }
 #endif
-              tmem_st32(a0 + lane_addr + 32 * kh, r);
+              MESW_PROF(dprof[2] += clock64() - dq;)
+              MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 2] = clock64();)
+              MESW_PROF(dq = clock64();)
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {  // the group's 4 warps of each CTA -> leader's afull (8 arrivals)
+                if (rank == 0) mbar_arrive(&S.afull[aslot]);
+                else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
+              }
+              if (++pos == na) { pos = 0; ++use; }
+              MESW_PROF(dprof[3] += clock64() - dq;)
+              MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 3] = clock64();)
+              MESW_PROF(dprof[7]++;)
             }
-#endif
-            MESW_PROF(dprof[2] += clock64() - dq;)
-            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 2] = clock64();)
-            MESW_PROF(dq = clock64();)
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {  // the group's 4 warps of each CTA -> leader's afull (8 arrivals)
-              if (rank == 0) mbar_arrive(&S.afull[aslot]);
-              else mbar_arrive_cta_relaxed(&S.afull[aslot], 0);
-            }
-            MESW_PROF(dprof[3] += clock64() - dq;)
-            MESW_PROF(if (jst) p.tbuf[4096 * 56 + 512 + 256 + grp * 128 + 4 * dprof[7] + 3] = clock64();)
-            MESW_PROF(dprof[7]++;)
+            mbar_arrive(&S.cempty[sc]);  // every thread: release orders its own smem reads
+            if (++sc == p.nc) { sc = 0; pc ^= 1; }
+            MESW_PROF(if (p.tbuf && blockIdx.x == 0 && threadIdx.x == kDqWarp0 * 32 + grp * 128 && dcount < 64) p.tbuf[4096 * 56 + 128 + grp * 64 + dcount] = clock64();)
+            MESW_PROF(++dcount;)
           }
-          mbar_arrive(&S.cempty[sc]);  // every thread: release orders its own smem reads
-          if (++sc == p.nc) { sc = 0; pc ^= 1; }
-          MESW_PROF(if (p.tbuf && blockIdx.x == 0 && threadIdx.x == kDqWarp0 * 32 + grp * 128 && dcount < 64) p.tbuf[4096 * 56 + 128 + grp * 64 + dcount] = clock64();)
-          MESW_PROF(++dcount;)
         }
       }
     }
@@ -1311,52 +1324,41 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   if (smem > 232448) return mesw_fail(MESW_ERR_UNSUPPORTED, "shared memory overflow");
   smem = 232448;  // one CTA per SM regardless: the slack stages the final stream-K reduction
   p.ring_bytes = (int)(smem - ring_offset());
-  // TMEM: n_acc buffers of [D_base NP | D_delta NP] columns, then the A ring (64-col job slots)
-  // MMA issuers (seg_issuer): the base tile on issuer 0, segments on the others.  Each
-  // issuer with delta jobs owns an A sub-ring (>= 1 slot of 64 TMEM columns); prefer two
-  // accumulator buffers, then more issuers.
+  // TMEM: n_acc buffers of [D_base NP | D_delta NP] columns, then the A ring (64-col job slots).
+  // Issuers: the base tile on warp role 0 (when there is a base), then n_dq <= 2 delta issuers;
+  // segment q goes to delta issuer q % n_dq, fed by dequant group q % n_dq.  Each delta
+  // issuer owns an A sub-ring of >= 1 slot (slots split by job count); prefer two
+  // accumulator buffers, then more delta issuers.
   {
-    int want = (p.w ? 1 : 0) + p.n_seg;
-    static const int env_iss = getenv("MESW_ISS") ? atoi(getenv("MESW_ISS")) : 0;
-    if (env_iss > 0) want = std::min(want, env_iss);
-    want = std::max(1, std::min(want, kMaxIssuers));
-    bool done = false;
+    static const int env_iss = getenv("MESW_ISS") ? atoi(getenv("MESW_ISS")) : 0;  // cap on delta issuers
     static const int nacc_max = getenv("MESW_NACC") ? atoi(getenv("MESW_NACC")) : 2;
     static const int env_maxslots = getenv("MESW_MAXSLOTS") ? atoi(getenv("MESW_MAXSLOTS")) : 0;
+    int nd_max = std::min(p.n_seg, kDqGroups);
+    if (env_iss > 0) nd_max = std::min(nd_max, env_iss);
+    const int r0 = p.w ? 1 : 0;
+    bool done = false;
     for (int n_acc = nacc_max; n_acc >= 1 && !done; --n_acc) {
-      for (int iss = want; iss >= 1 && !done; --iss) {
-        int n_delta = 0;  // issuers that own at least one segment
-        for (int i = 0; i < iss; ++i) {
-          bool any = false;
-          for (int q = 0; q < p.n_seg; ++q) any |= (seg_issuer(q, iss, p.w != nullptr) == i);
-          n_delta += any ? 1 : 0;
-        }
+      for (int nd = nd_max; nd >= (p.n_seg > 0 ? 1 : 0) && !done; --nd) {
         const int cols = kTmemCols - n_acc * 2 * p.NP;
         int slots = cols / kAColsPerSlot;
         if (slots > kMaxASlots) slots = kMaxASlots;
         if (env_maxslots > 0 && slots > env_maxslots) slots = env_maxslots;
-        if (cols < 0 || slots < n_delta) continue;
-        // every issuer with delta jobs gets >= 1 slot; the rest go to the most loaded
-        int jobs[3] = {0, 0, 0};
-        for (int q = 0; q < p.n_seg; ++q) jobs[seg_issuer(q, iss, p.w != nullptr)]++;
-        for (int i = 0; i < 3; ++i) { p.a_base[i] = 0; p.a_na[i] = (i < iss && jobs[i] > 0) ? 1 : 0; }
-        for (int left = slots - n_delta; left > 0; --left) {
-          int best = -1;
-          for (int i = 0; i < iss; ++i)
-            if (jobs[i] > 0 && (best < 0 || jobs[i] * p.a_na[best] > jobs[best] * p.a_na[i])) best = i;
-          if (best < 0) break;
-          p.a_na[best]++;
+        if (cols < 0 || slots < nd) continue;
+        for (int i = 0; i < 3; ++i) { p.a_base[i] = 0; p.a_na[i] = 0; }
+        int jobs[2] = {0, 0};
+        for (int q = 0; q < p.n_seg; ++q) jobs[q % nd]++;
+        for (int g = 0; g < nd; ++g) p.a_na[r0 + g] = 1;
+        for (int left = slots - nd; left > 0; --left) {  // next slot to the issuer with most jobs per slot
+          int best = 0;
+          for (int g = 1; g < nd; ++g)
+            if (jobs[g] * p.a_na[r0 + best] > jobs[best] * p.a_na[r0 + g]) best = g;
+          p.a_na[r0 + best]++;
         }
-        // dequant groups are slot-affine (slot s -> group s % 2): an odd sub-ring of >= 3 slots
-        // hands one group more of that issuer's jobs (3 slots: 2/3 of them), so round it down
-        static const bool even_slots = getenv("MESW_ODD_SLOTS") == nullptr;
-        if (even_slots && kDqGroups == 2)
-          for (int i = 0; i < 3; ++i)
-            if (p.a_na[i] > 1 && (p.a_na[i] & 1)) p.a_na[i]--;
         int base = 0;
         for (int i = 0; i < 3; ++i) { p.a_base[i] = base; base += p.a_na[i]; }
         p.n_acc = n_acc;
-        p.n_iss = iss;
+        p.n_dq = nd;
+        p.n_iss = std::max(1, r0 + nd);
         p.n_aslots = base;
         p.a_col0 = kTmemCols - base * kAColsPerSlot;
         done = true;

@@ -16,7 +16,7 @@
 namespace mesw {
 
 constexpr int kRouterBuckets = 1 << 16;
-constexpr int kRouterMaxDomains = 6;
+constexpr int kRouterMaxDomains = 32;  // one lane per domain
 constexpr int kRouterWarps = 4;  // queries per block
 
 __device__ __forceinline__ uint32_t fnv_byte(uint32_t h, uint32_t b) { return (h ^ b) * 16777619u; }
@@ -92,7 +92,7 @@ using namespace mesw;
 extern "C" int mesw_router_classify(const int32_t* d_codepoints, const int64_t* d_offsets, int B,
                                     const float* d_loglik, const float* d_logprior, int D, int32_t* d_domain,
                                     float* d_conf, int32_t* d_prior_only, void* stream) {
-  if (B < 0 || D < 1 || D > kRouterMaxDomains) return mesw_fail(MESW_ERR_VALUE, "router: 1..6 domains");
+  if (B < 0 || D < 1 || D > kRouterMaxDomains) return mesw_fail(MESW_ERR_VALUE, "router: 1..32 domains");
   if (!d_offsets || !d_loglik || !d_logprior || !d_domain || !d_conf)
     return mesw_fail(MESW_ERR_VALUE, "router: null buffer");
   if (B == 0) return MESW_OK;

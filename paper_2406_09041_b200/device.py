@@ -94,8 +94,14 @@ class DeviceDelta:
 
     @classmethod
     def from_blocks(cls, blocks: list, geom: LinearGeometry | None = None, device="cuda",
-                    stream=None) -> "DeviceDelta":
-        """Upload + repack MESW layer blocks (one per output block) into the device layout."""
+                    stream=None, staging: list | None = None) -> "DeviceDelta":
+        """Upload + repack MESW layer blocks (one per output block) into the device layout.
+
+        Host bytes are staged in pinned buffers and copied asynchronously on `stream` (the
+        registry's copy stream), where the K1 repack kernels run too.  With a stream, the
+        pinned buffers are appended to `staging` and must stay alive until the stream has
+        been synchronised (the caller does that once per expert); without one, the call
+        synchronises the current stream itself."""
         L = _lib.lib()
         blocks = list(blocks)
         if geom is None:
@@ -106,30 +112,60 @@ class DeviceDelta:
         for b, nb in zip(blocks, geom.block_n):
             if b.rows != geom.m or b.cols != nb:
                 raise ValueError(f"block shape {(b.rows, b.cols)} != geometry {(geom.m, nb)}")
+            if b.salient.k and int(np.asarray(b.salient.indices)[-1]) >= b.rows:
+                # reference: reconstruct() indexes the dense delta with them (compress.py:119-120)
+                raise IndexError(f"salient index {int(np.asarray(b.salient.indices)[-1])} out of range "
+                                 f"for {b.rows} input channels")
             if b.bits != bits:
                 raise NotImplementedError("mixed bit widths inside one fused linear")
         db = L.mesw_device_code_bits(bits)
         if db == 0:
             raise ValueError(f"bits must be one of (1, 2, 3, 4, 8), got {bits}")
         dev = torch.device(device)
-        s = _stream(stream)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        stage = staging if staging is not None else []
+
+        def h2d(host: torch.Tensor) -> torch.Tensor:  # pinned staging + async copy on `st`
+            pinned = host.pin_memory()
+            stage.append(pinned)
+            return pinned.to(dev, non_blocking=True)
+
         m_pad, n_pad = geom.m_pad, geom.n_pad
-        codes = torch.empty(int(L.mesw_codes_device_bytes(m_pad, n_pad, db)), dtype=torch.uint8, device=dev)
-        steps = torch.zeros(n_pad, dtype=torch.float32, device=dev)
-        for b, cb in zip(blocks, geom.col_base):
-            idx = torch.as_tensor(np.ascontiguousarray(b.salient.indices, dtype=np.int32)).to(dev)
-            packed = torch.frombuffer(bytearray(b.packed.data), dtype=torch.uint8) if b.packed.data else \
-                torch.zeros(1, dtype=torch.uint8)
-            packed = packed.to(dev)
-            _lib.check(L.mesw_repack_codes(packed.data_ptr(), b.rows, b.cols, bits, idx.data_ptr(),
-                                           b.salient.k, codes.data_ptr(), m_pad, n_pad, cb, s))
-            steps[cb:cb + b.cols] = torch.as_tensor(np.ascontiguousarray(b.steps, np.float32)).to(dev)
-        off, sidx, srows = build_salient_tables(blocks, geom)
-        d = cls(geom=geom, bits=bits, code_bits=db, codes=codes, steps=steps,
-                sal_off=off.to(dev), sal_idx=sidx.to(dev), sal_rows=srows.to(dev))
+        off, sidx, srows = build_salient_tables(blocks, geom)  # host; validates the salient indices
+        with torch.cuda.stream(st):
+            s = _stream(st)
+            codes = torch.empty(int(L.mesw_codes_device_bytes(m_pad, n_pad, db)), dtype=torch.uint8, device=dev)
+            steps_h = torch.zeros(n_pad, dtype=torch.float32)
+            for b, cb in zip(blocks, geom.col_base):
+                idx = h2d(torch.as_tensor(np.ascontiguousarray(b.salient.indices, dtype=np.int32)))
+                raw = np.frombuffer(b.packed.data, dtype=np.uint8) if b.packed.data else np.zeros(1, np.uint8)
+                packed = h2d(torch.from_numpy(raw.copy()))
+                _lib.check(L.mesw_repack_codes(packed.data_ptr(), b.rows, b.cols, bits, idx.data_ptr(),
+                                               b.salient.k, codes.data_ptr(), m_pad, n_pad, cb, s))
+                steps_h[cb:cb + b.cols] = torch.from_numpy(np.ascontiguousarray(b.steps, np.float32))
+            d = cls(geom=geom, bits=bits, code_bits=db, codes=codes, steps=h2d(steps_h),
+                    sal_off=h2d(off), sal_idx=h2d(sidx), sal_rows=h2d(srows))
         d.nbytes = sum(t.numel() * t.element_size() for t in (d.codes, d.steps, d.sal_off, d.sal_idx, d.sal_rows))
-        torch.cuda.current_stream(dev).synchronize() if stream is None else None
+        if stream is None:
+            st.synchronize()
         return d
+
+    @staticmethod
+    def device_nbytes(blocks: list, geom: LinearGeometry | None = None) -> int:
+        """HBM bytes `from_blocks(blocks, geom)` will occupy, computed on the host before
+        loading (the registry charges its budget in these device bytes): codes, steps and
+        the per-column-group salient tables."""
+        L = _lib.lib()
+        blocks = list(blocks)
+        if geom is None:
+            geom = LinearGeometry(blocks[0].rows, tuple(b.cols for b in blocks))
+        db = L.mesw_device_code_bits(blocks[0].bits)
+        rows = 0  # salient table rows: every column group of block b holds its k_b rows
+        for b, cb in zip(blocks, geom.col_base):
+            rows += b.salient.k * (_ceil(cb + b.cols) // TILE - cb // TILE)
+        rows = max(rows, 1)
+        return (int(L.mesw_codes_device_bytes(geom.m_pad, geom.n_pad, db)) + 4 * geom.n_pad
+                + 4 * (geom.n_cg + 1) + 4 * rows + 2 * TILE * rows)
 
     def descriptor(self) -> tuple:
         return (self.codes.data_ptr(), self.steps.data_ptr(), self.sal_off.data_ptr(),
@@ -171,12 +207,12 @@ def build_salient_tables(blocks: list, geom: LinearGeometry):
     idx_ptrs = (C.c_void_p * nb)(*[a.ctypes.data if a.size else None for a in idx_arrs])
     row_ptrs = (C.c_void_p * nb)(*[a.ctypes.data if a.size else None for a in row_arrs])
     total = C.c_uint64()
-    _lib.check(L.mesw_build_salient_tables(nb, col_base, ns, ks, idx_ptrs, row_ptrs, geom.n_pad,
+    _lib.check(L.mesw_build_salient_tables(geom.m, nb, col_base, ns, ks, idx_ptrs, row_ptrs, geom.n_pad,
                                            None, None, None, C.byref(total)))
     off = np.zeros(geom.n_cg + 1, np.int32)
     sidx = np.zeros(max(total.value, 1), np.int32)
     srows = np.zeros((max(total.value, 1), TILE), np.uint16)
-    _lib.check(L.mesw_build_salient_tables(nb, col_base, ns, ks, idx_ptrs, row_ptrs, geom.n_pad,
+    _lib.check(L.mesw_build_salient_tables(geom.m, nb, col_base, ns, ks, idx_ptrs, row_ptrs, geom.n_pad,
                                            off.ctypes.data, sidx.ctypes.data, srows.ctypes.data,
                                            C.byref(total)))
     return torch.from_numpy(off), torch.from_numpy(sidx), torch.from_numpy(srows.view(np.int16))

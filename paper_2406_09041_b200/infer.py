@@ -242,9 +242,16 @@ class ExpertSet:
         layers = artifact.layers if hasattr(artifact, "layers") else list(artifact)
         if len(layers) != self.base.n_weight_layers:
             raise ValueError("artifact layer count does not match the base model")
+        return self.add_device(expert_id, [DeviceDelta.from_blocks([layer], device=self.base.device)
+                                           for layer in layers])
+
+    def add_device(self, expert_id, deltas: list) -> int:
+        """Install already-resident per-layer DeviceDeltas (e.g. a registry handle's)."""
+        if len(deltas) != self.base.n_weight_layers:
+            raise ValueError("artifact layer count does not match the base model")
         slot = len(self.slots)
-        for t, layer in zip(self.tables, layers):
-            t.set(slot, DeviceDelta.from_blocks([layer], device=self.base.device))
+        for t, d in zip(self.tables, deltas):
+            t.set(slot, d)
         self.slots[expert_id] = slot
         return slot
 
@@ -264,14 +271,45 @@ def _precise_linear(x: torch.Tensor, pair, table: ExpertTable, segs) -> torch.Te
     return y2[:c] + y2[c:] + y3
 
 
-def batched_multi_model_forward(base: ToyBase, experts: ExpertSet, plan) -> list:
+def batched_multi_model_forward(base: ToyBase, registry, plan) -> list:
     """SPEC.md:433-438 on the GPU: shared-base x.W and every expert group's delta in
     fused launches per layer; per-query results in input order.
 
+    `registry` is the SPEC's registry handle (`registry.ExpertRegistry` whose loader returns
+    per-layer device deltas, e.g. `registry.GpuExpert`): every distinct expert of the plan
+    is acquired (loaded on demand, pinned) for the duration of the batch and released
+    afterwards with a fence on the stream that ran it.  An
+    `ExpertSet` of already-resident experts is accepted too.
+
     Returns [(query_id, logits f32 [len, V] or None, error or None)].  An unknown
-    expert yields an error entry for that query and the batch continues.
+    expert (or one that cannot be made resident) yields an error entry for that query
+    and the batch continues.
     """
     queries = plan.queries if isinstance(plan, BatchPlan) else tuple(plan)
+    if isinstance(registry, ExpertSet):
+        return _forward_resident(base, registry, queries)
+    from .errors import RegistryError
+    acquired, failed = [], {}
+    experts = ExpertSet(base)
+    try:
+        for eid in dict.fromkeys(q[1] for q in queries):  # distinct, first-seen order
+            try:
+                handle = registry.acquire(eid)
+            except RegistryError as e:  # UnknownExpertError, BudgetExceededError
+                failed[eid] = f"{type(e).__name__}: {e}"
+                continue
+            acquired.append(eid)
+            experts.add_device(eid, list(handle.layers))
+        res = _forward_resident(base, experts, queries)
+    finally:
+        stream = torch.cuda.current_stream(base.device)
+        for eid in acquired:
+            registry.release(eid, stream)
+    return [(qid, None, failed[queries[i][1]]) if queries[i][1] in failed else (qid, lg, err)
+            for i, (qid, lg, err) in enumerate(res)]
+
+
+def _forward_resident(base: ToyBase, experts: ExpertSet, queries) -> list:
     results = {}
     order = []
     for qi, (qid, eid, toks) in enumerate(queries):

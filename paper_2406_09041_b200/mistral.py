@@ -29,6 +29,7 @@ from .synth import MistralShape
 _FUSED_ROPE = os.environ.get("MESW_ROPE_SPLIT") is None
 
 PROJ_ORDER = ("q", "k", "v", "o", "gate", "up", "down")
+MAX_EXPERT_SLOTS = 128  # resident experts per engine (C5: 64 on one GPU)
 
 
 @dataclass
@@ -62,6 +63,10 @@ def _launch_groups(B: int, segs: list) -> list:
     return groups
 
 
+class CacheWindowError(ValueError):
+    """A decode step would write past a request's KV-cache window (ctx_max)."""
+
+
 class MistralMultiExpert:
     """Base model + resident experts + decode buffers for up to `max_batch` requests."""
 
@@ -82,7 +87,9 @@ class MistralMultiExpert:
         self.g_down = LinearGeometry(s.intermediate, (s.hidden,))
         self.g_head = LinearGeometry(s.hidden, (s.vocab,))
         self.layers: list[LayerWeights] = []
-        self.tables = [[ExpertTable(self.device) for _ in range(4)] for _ in range(self.n_layers)]
+        # fixed capacity: launch plans bind the tables' device pointers (a table never regrows here)
+        self.tables = [[ExpertTable(self.device, capacity=MAX_EXPERT_SLOTS) for _ in range(4)]
+                       for _ in range(self.n_layers)]
         self.experts: dict = {}
         self.embedding = None
         self.final_norm = None
@@ -90,6 +97,12 @@ class MistralMultiExpert:
         self._alloc_buffers()
         self.graph = None
         self._plans = None
+        # benchmark steady state only: a request reaching ctx_max wraps back to position 128
+        # (its cache rows are overwritten).  Serving (False) raises CacheWindowError instead.
+        self.wrap_positions = False
+        self._pos_max = 0
+        self.registry = None
+        self._pinned = []
 
     # ------------------------------------------------------------------ weights
     def _alloc_buffers(self):
@@ -172,29 +185,95 @@ class MistralMultiExpert:
         return n + self.head.frag.numel() * 2
 
     # ------------------------------------------------------------------ experts
-    def add_expert(self, expert_id, artifact) -> int:
-        """Make an expert resident: its artifact holds 7 blocks per layer (q,k,v,o,gate,up,down)."""
+    def _fused_blocks(self, artifact) -> list:
+        """Per layer: the blocks of the 4 fused linears (q|k|v, o, gate|up, down) with their geometry."""
         layers = artifact.layers if hasattr(artifact, "layers") else list(artifact)
         if len(layers) != 7 * self.n_layers:
             raise ValueError(f"expert artifact has {len(layers)} blocks, expected {7 * self.n_layers}")
-        slot = len(self.experts)
-        nbytes = 0
+        out = []
         for l in range(self.n_layers):
             blk = dict(zip(PROJ_ORDER, layers[7 * l:7 * l + 7]))
-            deltas = [DeviceDelta.from_blocks([blk["q"], blk["k"], blk["v"]], self.g_qkv, self.device),
-                      DeviceDelta.from_blocks([blk["o"]], self.g_o, self.device),
-                      DeviceDelta.from_blocks([blk["gate"], blk["up"]], self.g_gu, self.device),
-                      DeviceDelta.from_blocks([blk["down"]], self.g_down, self.device)]
-            for t, d in zip(self.tables[l], deltas):
+            out.append((([blk["q"], blk["k"], blk["v"]], self.g_qkv), ([blk["o"]], self.g_o),
+                        ([blk["gate"], blk["up"]], self.g_gu), ([blk["down"]], self.g_down)))
+        return out
+
+    def load_deltas(self, artifact, stream=None) -> list:
+        """Upload + repack an expert (pinned staging, async copies and K1 on `stream`):
+        [layer][linear kind] DeviceDelta."""
+        staging: list = []
+        deltas = [[DeviceDelta.from_blocks(b, g, self.device, stream=stream, staging=staging) for b, g in kinds]
+                  for kinds in self._fused_blocks(artifact)]
+        (stream if stream is not None else torch.cuda.current_stream(self.device)).synchronize()
+        return deltas
+
+    def expert_device_bytes(self, artifact) -> int:
+        """HBM bytes an expert will occupy in this engine (the registry budget unit)."""
+        return sum(DeviceDelta.device_nbytes(b, g) for kinds in self._fused_blocks(artifact) for b, g in kinds)
+
+    def _install(self, expert_id, deltas) -> int:
+        used = {sl for sl, _ in self.experts.values()}
+        slot = next(i for i in range(len(used) + 1) if i not in used)  # lowest free slot
+        if slot >= MAX_EXPERT_SLOTS:
+            raise ValueError(f"more than {MAX_EXPERT_SLOTS} resident experts")
+        nbytes = 0
+        for l, per in enumerate(deltas):
+            for t, d in zip(self.tables[l], per):
                 t.set(slot, d)
                 nbytes += d.nbytes
         self.experts[expert_id] = (slot, nbytes)
+        return slot
+
+    def _uninstall(self, expert_id) -> None:
+        slot, _ = self.experts.pop(expert_id)
+        for per in self.tables:
+            for t in per:
+                t.set(slot, None)
+
+    def add_expert(self, expert_id, artifact) -> int:
+        """Make an expert resident: its artifact holds 7 blocks per layer (q,k,v,o,gate,up,down)."""
+        slot = self._install(expert_id, self.load_deltas(artifact))
         self._plans = None
         self.graph = None
         return slot
 
     def expert_bytes(self) -> int:
         return sum(nb for _, nb in self.experts.values())
+
+    # ------------------------------------------------------------------ registry (on-demand experts)
+    def make_registry(self, budget_bytes: int, base_digest: str):
+        """An `ExpertRegistry` that owns this engine's expert residency:
+        `set_batch` acquires (loads on demand, pins) the batch's experts and releases the
+        previous batch's with a fence on the decode stream; eviction (strict LRU over
+        unpinned experts) waits for that fence, then frees the expert's table slot.  The
+        budget counts HBM bytes (`expert_device_bytes`); loads run on a copy stream from
+        pinned host buffers."""
+        from .registry import ExpertRegistry, GpuHandle
+
+        eng = self
+
+        class EngineExpert(GpuHandle):
+            def __init__(self, deltas):
+                self.deltas = deltas
+                self.device_bytes = sum(d.nbytes for per in deltas for d in per)
+
+        def load(expert_id, artifact):
+            h = EngineExpert(eng.load_deltas(artifact, stream=eng._copy_stream()))
+            eng._install(expert_id, h.deltas)
+            return h
+
+        def unload(expert_id, handle):
+            if expert_id in eng.experts:
+                eng._uninstall(expert_id)
+
+        self.registry = ExpertRegistry(budget_bytes, base_digest, loader=load, unloader=unload,
+                                       size_fn=self.expert_device_bytes)
+        self._pinned = []
+        return self.registry
+
+    def _copy_stream(self):
+        if getattr(self, "_cstream", None) is None:
+            self._cstream = torch.cuda.Stream(device=self.device)
+        return self._cstream
 
     # ------------------------------------------------------------------ batch
     def set_batch(self, expert_ids: list, prompt_lens: list | None = None) -> np.ndarray:
@@ -206,6 +285,22 @@ class MistralMultiExpert:
         n = len(expert_ids)
         if n < 1:
             raise ValueError("empty batch")
+        reg = getattr(self, "registry", None)
+        if reg is not None:  # on-demand residency: pin this batch's experts, unpin the last batch's
+            want = list(dict.fromkeys(e for e in expert_ids if e is not None))
+            stream = torch.cuda.current_stream(self.device)
+            for e in self._pinned:
+                reg.release(e, stream)
+            self._pinned = []
+            try:
+                for e in want:
+                    reg.acquire(e)
+                    self._pinned.append(e)
+            except BaseException:
+                for e in self._pinned:
+                    reg.release(e, stream)
+                self._pinned = []
+                raise
         slots = []
         for e in expert_ids:
             if e is None:
@@ -244,6 +339,7 @@ class MistralMultiExpert:
         self.segments = segs
         self.pos[:B] = torch.as_tensor(pl, dtype=torch.int32)
         self.len[:B] = torch.as_tensor(pl + 1, dtype=torch.int32)
+        self._pos_max = int(pl.max())
         return rows
 
     def fill_random_kv(self, prompt_len: int, seed: int = 1) -> None:
@@ -307,10 +403,14 @@ class MistralMultiExpert:
         sms = Workspace.get(self.device).sms
         return tune_num_ctas(key, make, cta_candidates(weight.geom, sms))
 
-    def step(self, stream=None) -> None:
+    def step(self, stream=None, trace=None) -> None:
         """One decode step for the whole batch: ids (engine order) -> next ids in self.ids.
         Batches wider than one fused launch (> MAX_ROWS padded rows, e.g. many experts)
-        run as several launch groups; each re-streams the base weights."""
+        run as several launch groups; each re-streams the base weights.
+
+        trace (parity checks, eager only): called as trace(when, kind, layer, r0, r1, bufs)
+        with when in ("pre", "post") around every fused linear launch (kind in "qkv", "o",
+        "gu", "down", "head"), so a checker can read the exact bf16 inputs and outputs."""
         if self._plans is None:
             self._build_plans()
         L = _lib.lib()
@@ -334,7 +434,11 @@ class MistralMultiExpert:
             for (r0, r1, bufs, layers, _) in self._plans:
                 chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), lw.attn_norm.data_ptr(), r1 - r0, H, eps,
                                    bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "xn"), st))
+                if trace:
+                    trace("pre", "qkv", l, r0, r1, bufs)
                 layers[l][0](stream)
+                if trace:
+                    trace("post", "qkv", l, r0, r1, bufs)
             kc, vc = self.kcache[l], self.vcache[l]
             if not _FUSED_ROPE:  # two-call form (A/B switch MESW_ROPE_SPLIT=1)
                 chk(L.mesw_rope_append(self.qkv.data_ptr(), self.qkv.stride(0), self.pos.data_ptr(), B, s.n_heads,
@@ -353,22 +457,38 @@ class MistralMultiExpert:
                                                 s.n_kv_heads, s.head_dim, self.ctx_max, bufs["attn"].data_ptr(), 0,
                                                 canonical_rows(r1 - r0), self.attn_ws.data_ptr(),
                                                 self.attn_ws.numel(), *corr(bufs, "attn"), st))
+                if trace:
+                    trace("pre", "o", l, r0, r1, bufs)
                 layers[l][1](stream)
+                if trace:
+                    trace("post", "o", l, r0, r1, bufs)
             for (r0, r1, bufs, layers, _) in self._plans:
                 chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), lw.mlp_norm.data_ptr(), r1 - r0, H, eps,
                                    bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "xn"), st))
+                if trace:
+                    trace("pre", "gu", l, r0, r1, bufs)
                 layers[l][2](stream)
+                if trace:
+                    trace("post", "gu", l, r0, r1, bufs)
             for (r0, r1, bufs, layers, _) in self._plans:
                 chk(L.mesw_swiglu(rows_ptr(self.gu, r0), self.gu.stride(0), r1 - r0, s.intermediate,
                                   bufs["act"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "act"), st))
+                if trace:
+                    trace("pre", "down", l, r0, r1, bufs)
                 layers[l][3](stream)
+                if trace:
+                    trace("post", "down", l, r0, r1, bufs)
         for (r0, r1, bufs, _, head) in self._plans:
             chk(L.mesw_rmsnorm(rows_ptr(self.h, r0), self.h.stride(0), self.final_norm.data_ptr(), r1 - r0, H, eps,
                                bufs["xn"].data_ptr(), 0, canonical_rows(r1 - r0), None, 0, st))
+            if trace:
+                trace("pre", "head", -1, r0, r1, bufs)
             head(stream)
+            if trace:
+                trace("post", "head", -1, r0, r1, bufs)
         chk(L.mesw_argmax(self.logits.data_ptr(), 1, B, s.vocab, self.logits.stride(0), self.ids.data_ptr(), st))
-        chk(L.mesw_advance_positions(self.pos.data_ptr(), self.len.data_ptr(), B, self.ctx_max,
-                                     min(self.ctx_max - 1, 128), st))
+        wrap_to = min(self.ctx_max - 1, 128) if self.wrap_positions else -1
+        chk(L.mesw_advance_positions(self.pos.data_ptr(), self.len.data_ptr(), B, self.ctx_max, wrap_to, st))
 
     def launches_per_step(self) -> int:
         g = len(self.groups)
@@ -376,8 +496,16 @@ class MistralMultiExpert:
         return 1 + per_layer * self.n_layers + g * 2 + 2
 
     def capture(self) -> None:
-        """Capture one decode step in a CUDA graph (replayed by `replay`)."""
+        """Capture one decode step in a CUDA graph (replayed by `replay`).  The warm-up step
+        (kernel attributes, launch-width tuning) runs eagerly, so the decode state it
+        advances -- ids, positions, lengths -- is restored afterwards; the KV row it wrote
+        is rewritten by the next real step at the same position."""
+        B = self.B
+        saved = (self.ids[:B].clone(), self.pos[:B].clone(), self.len[:B].clone())
         self.step()  # warm: configures kernel attributes outside capture
+        self.ids[:B].copy_(saved[0])
+        self.pos[:B].copy_(saved[1])
+        self.len[:B].copy_(saved[2])
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(device=self.device)
@@ -389,9 +517,18 @@ class MistralMultiExpert:
         torch.cuda.current_stream(self.device).wait_stream(s)
         self.graph = g
 
+    def _advance_host(self) -> None:
+        """Host-side cache-window check before a step (positions advance on the device)."""
+        if not self.wrap_positions:
+            if self._pos_max >= self.ctx_max:
+                raise CacheWindowError(f"a request reached the cache window (ctx_max={self.ctx_max}); "
+                                       "finish or re-batch it before the next step")
+            self._pos_max += 1
+
     def replay(self) -> None:
         if self.graph is None:
             self.capture()
+        self._advance_host()
         self.graph.replay()
 
     def bytes_per_step(self) -> dict:

@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 from . import compress
 from .errors import (BaseDigestMismatchError, BudgetExceededError, DuplicateExpertError, UnknownExpertError)
 
-__all__ = ["RegistryEntry", "ResidencyState", "ExpertRegistry", "GpuExpert", "gpu_loader"]
+__all__ = ["RegistryEntry", "ResidencyState", "ExpertRegistry", "GpuHandle", "GpuExpert", "gpu_loader"]
 
 
 @dataclass(frozen=True)
@@ -54,19 +54,46 @@ class _Slot:
     error: BaseException | None = None
 
 
-class GpuExpert:
-    """An expert's deltas resident in HBM: one DeviceDelta per MESW layer block."""
+class GpuHandle:
+    """Residency handle with a consumer fence.  `fence(stream)` (called by `release`)
+    records an event on the stream whose kernels read the expert's buffers; eviction
+    calls `wait_idle()` before the buffers are dropped, so a kernel still queued on a
+    decode stream never reads freed (and possibly re-allocated) memory."""
+
+    _events: list
+
+    def fence(self, stream=None) -> None:
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(stream if stream is not None else torch.cuda.current_stream())
+        self._events = [ev]  # stream order: the latest event covers the earlier ones
+
+    def wait_idle(self) -> None:
+        for ev in getattr(self, "_events", []):
+            ev.synchronize()
+        self._events = []
+
+
+class GpuExpert(GpuHandle):
+    """An expert's deltas resident in HBM: one DeviceDelta per MESW layer block, uploaded
+    from pinned host buffers on a dedicated copy stream (K1 repack runs there too)."""
 
     def __init__(self, artifact, device="cuda"):
         import torch
         from .device import DeviceDelta
         self.manifest = artifact.manifest
         self.stream = torch.cuda.Stream(device=device)  # copy + repack off the decode stream
-        with torch.cuda.stream(self.stream):
-            self.layers = [DeviceDelta.from_blocks([blk], device=device, stream=self.stream)
-                           for blk in artifact.layers]
-        self.stream.synchronize()
+        staging: list = []
+        self.layers = [DeviceDelta.from_blocks([blk], device=device, stream=self.stream, staging=staging)
+                       for blk in artifact.layers]
+        self.stream.synchronize()  # the pinned staging buffers are free after this
+        del staging
         self.device_bytes = sum(d.nbytes for d in self.layers)
+
+    @staticmethod
+    def planned_bytes(artifact) -> int:
+        from .device import DeviceDelta
+        return sum(DeviceDelta.device_nbytes([blk]) for blk in artifact.layers)
 
 
 def gpu_loader(expert_id, artifact):
@@ -81,13 +108,18 @@ def _read(source) -> bytes:
 
 
 class ExpertRegistry:
-    def __init__(self, budget_bytes: int, base_digest: str, loader=gpu_loader, unloader=None):
+    """`size_fn(artifact) -> bytes` sets what the budget counts: the SPEC's artifact bytes
+    (`compressed_size_bytes`, the default) or the HBM bytes the loader will allocate
+    (`GpuExpert.planned_bytes`, or the serving engine's `MistralMultiExpert.expert_device_bytes`)."""
+
+    def __init__(self, budget_bytes: int, base_digest: str, loader=gpu_loader, unloader=None, size_fn=None):
         if budget_bytes <= 0:
             raise ValueError("budget_bytes must be positive")
         self.budget = int(budget_bytes)
         self.base_digest = base_digest
         self._loader = loader
         self._unloader = unloader
+        self._size_fn = size_fn
         self._lock = threading.Lock()
         self._entries: dict = {}
         self._slots: dict = {}
@@ -106,7 +138,7 @@ class ExpertRegistry:
             raise BaseDigestMismatchError(
                 f"expert {expert_id!r} was compressed against base {art.manifest.base_digest[:12]}…, "
                 f"registry base is {self.base_digest[:12]}…")
-        size = compress.compressed_size_bytes(art).total
+        size = int(self._size_fn(art)) if self._size_fn is not None else compress.compressed_size_bytes(art).total
         entry = RegistryEntry(expert_id, art.manifest.domain, size, source)
         with self._lock:
             if expert_id in self._entries:
@@ -154,6 +186,8 @@ class ExpertRegistry:
                 loading = None
         if loading is None:  # we own the load: evict, read and upload outside the lock
             for k, s in evicted:
+                if hasattr(s.handle, "wait_idle"):
+                    s.handle.wait_idle()  # kernels queued before its last release have finished
                 if self._unloader is not None:
                     self._unloader(k, s.handle)
                 s.handle = None
@@ -175,11 +209,16 @@ class ExpertRegistry:
                 raise slot.error
         return slot.handle
 
-    def release(self, expert_id: str) -> None:
+    def release(self, expert_id: str, stream=None) -> None:
+        """Unpin.  For GPU handles, `stream` is the stream the caller's kernels that read
+        the expert were queued on (default: the current stream): an event recorded there
+        is what eviction waits for."""
         with self._lock:
             slot = self._slots.get(expert_id)
             if slot is None or slot.pins == 0:
                 raise UnknownExpertError(f"expert {expert_id!r} is not acquired")
+            if hasattr(slot.handle, "fence"):
+                slot.handle.fence(stream)
             slot.pins -= 1
 
     def stats(self) -> ResidencyState:

@@ -21,7 +21,8 @@ __all__ = ["Router", "train_router", "save_router", "load_router", "DeviceRouter
            "classify_batch", "evaluate_router", "render_prompt", "ngram_buckets", "N_BUCKETS"]
 
 N_BUCKETS = 1 << 16
-MAX_DOMAINS = 6
+MAX_DOMAINS = 32  # classification: one warp lane per domain (K4); the prompt template caps at 6
+PROMPT_MAX_OPTIONS = 6  # render_prompt enumerates A..F
 MERT_MAGIC = b"MERT"
 MERT_VERSION = 1
 
@@ -118,7 +119,7 @@ def load_router(blob: bytes) -> Router:
 
 
 class DeviceRouter:
-    """Router tables resident on the GPU (1.5 MiB at 6 domains: L2-resident)."""
+    """Router tables resident on the GPU (256 KiB per domain: 4 MiB at 16 domains, L2-resident)."""
 
     def __init__(self, router: Router, device="cuda"):
         import torch
@@ -191,7 +192,7 @@ _TEMPLATE_HEAD = ("Classify the query based on the required expertise. Route the
 def render_prompt(query: str, domains) -> str:
     """The paper's routing prompt (Appendix A, Table A) with lettered options."""
     domains = list(domains)
-    if len(domains) > MAX_DOMAINS:
+    if len(domains) > PROMPT_MAX_OPTIONS:
         raise ValueError("the template enumerates at most 6 options (A..F)")
     opts = " ".join(f"{chr(65 + i)}) {name} - {desc}" for i, (name, desc) in enumerate(domains))
     letters = ", ".join(f"'{chr(65 + i)}'" for i in range(len(domains)))
