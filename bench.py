@@ -11,6 +11,12 @@ Workloads (BASELINE.json configs):
   c5: 64 experts sharded over the N GPUs (64/N per GPU, expert e on rank e mod N), batch 128
       per GPU through the c2 decode engine (with --gpus 1 all 64 experts are resident on one GPU).
 
+The default c2 line (N=1) also carries, measured in the same process outside the timed
+region: `c1` (the C1 kernel line), `c3` (16 router-assigned experts, B=128), `parity`
+(sampled layer vs the f64 restatement), `delta_gemm` (delta-only launches), `router`.
+
+--gpus N without WORLD_SIZE re-launches itself under torchrun (one process per GPU).
+
 Under torchrun (N>1) every rank serves its own expert shard (experts placed e mod G,
 replicated base, no collective on the data path): weak scaling, value = all tokens / max time.
 """
@@ -104,9 +110,18 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--experts", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="c2 only: skip the same-process C1/C3/parity legs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver does the same)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MESW_MASTER_PORT", "29517"),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if ws != args.gpus:
+        print(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE={ws}; using {ws} rank(s)", file=sys.stderr)
 
     if args.impl == "reference":
         from bench_impl import reference_arm
@@ -121,6 +136,8 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        print(f"[bench] rank {rank}/{ws} on cuda:{local} ({torch.cuda.get_device_name(local)}), "
+              f"process group size {dist.get_world_size()}", file=sys.stderr, flush=True)
     from bench_impl import run_ours
     line = run_ours(args, ws, rank, local, ClockSampler, _peaks)
     if rank == 0:

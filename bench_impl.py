@@ -142,6 +142,32 @@ def _device_c1(torch, W, arts, replicas: int):
     return sets
 
 
+def c1_leg(args, peaks):
+    """BASELINE config 1 as an extra key of the default line (same process): kernel time,
+    GB/s and roofline fraction of the fused linear, plus its delta-only (delta-GEMM) launch."""
+    import argparse
+    a = argparse.Namespace(**vars(args))
+    a.no_cpu_baseline = True
+    line = run_c1(a, 1, 0, 0, _NoClocks, peaks)
+    return {"workload": line["config"]["workload"], "us_per_launch": line["ms_per_step"] * 1e3,
+            "value": line["value"], "unit": "tokens/s", "roofline": line["roofline"],
+            "delta_gemm": line["delta_gemm"], "e2e": line["e2e"], "num_ctas": line["config"]["num_ctas"]}
+
+
+class _NoClocks:
+    def __init__(self, *a):
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+    def summary(self):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["sampled by the main line"]}
+
+
 def run_c1(args, ws, rank, local, ClockSampler, peaks):
     import torch
     from paper_2406_09041_b200 import synth
@@ -212,6 +238,20 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
     peak, peak_kind = peaks()
     achieved = bytes_launch / (per_step / 1e3) / 1e9
 
+    # delta-GEMM: the same launches without the base weight (codes + salient + steps only)
+    dplans = [LinearPlan(xc, rows, None, table, asegs, ya, x_corr=corr, num_ctas=ctas) for _, table in sets]
+    for i in range(args.warmup):
+        dplans[i % replicas]()
+    torch.cuda.synchronize()
+    st.record(stream)
+    for i in range(args.steps):
+        dplans[i % replicas]()
+    en.record(stream)
+    torch.cuda.synchronize()
+    d_us = st.elapsed_time(en) * 1e3 / args.steps
+    d_bytes = synth.linear_bytes(C1_M, C1_N, C1_E, C1_B, base=False)
+    d_gbs = d_bytes / (d_us / 1e6) / 1e9
+
     # e2e through the public API: pinned host x -> device, fused linear, y -> pinned host
     xh = torch.from_numpy(x_np[order]).to(torch.bfloat16).pin_memory()
     yh = torch.empty((C1_B, C1_N), dtype=torch.bfloat16).pin_memory()
@@ -243,6 +283,8 @@ def run_c1(args, ws, rank, local, ClockSampler, peaks):
                      "bytes_per_launch": bytes_launch, "kernel": "me_linear_tc_kernel<2, true> (cta_group::2 pairs, offset-form codes)"},
         "e2e": {"value": ws * C1_B / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(xh.numel() * 2),
                 "d2h_bytes_per_step": int(yh.numel() * 2)},
+        "delta_gemm": {"bytes_per_launch": d_bytes, "us_per_launch": d_us, "gbs": d_gbs, "frac": d_gbs / peak,
+                       "note": "delta-only launch (no base weight) over the same 3 experts / rows"},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }

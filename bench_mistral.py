@@ -1,16 +1,19 @@
-"""C2/C3 workload for bench.py: Mistral-7B-shaped multi-expert decode.
+"""C2/C3/C5 workloads for bench.py: Mistral-7B-shaped multi-expert decode.
 
-GPU arm: full 32-layer stack, E synthetic experts (2-bit codes + 8 fp16 salient rows
-on all 224 decoder linears), batch of B requests assigned round-robin to experts,
-128-token synthetic prompt state (random KV), one step = one generated token per
-request.  The step is a CUDA graph of libmesw.so kernels only.
+GPU arm: full 32-layer stack, E synthetic experts (2-bit codes + 8 fp16 salient rows on
+all 224 decoder linears).  Requests are ROUTER-ASSIGNED: rank 0 synthesises one query per
+request from per-domain keyword pools, the batched GPU router (K4) classifies them, and
+the domain index is the expert id; requests go to the expert's owner rank through
+`shard.ShardedService` (a host control message -- no data collective).  128-token
+synthetic prompt state (random KV); one step = one generated token per request; the step
+is a CUDA graph of libmesw.so kernels only.
 
-CPU arm (cpu_baseline / --impl reference): the reference algorithm restated in
-numpy (oracle port; the reference is Python and is absent on the GPU box): shared
-base x@W for the batch, then per expert group x_g @ reconstruct() with the dense
-delta cached (the reference's best case; as shipped it re-decodes every call),
-plus RMSNorm / RoPE / attention / SwiGLU glue.  Timed on a bounded sample -- one
-decoder layer -- and scaled to the 32-layer step (+ lm_head).
+Extra legs of the default (N=1, c2) line, measured in the same process outside the timed
+region: SPEC bench_decode decomposition (base-only / delta-only / fused linears ->
+delta-GEMM GB/s), sampled-layer parity against the f64 restatement, the C1 kernel line
+and the C3 line (16 router-assigned experts, B = 128).
+
+CPU arm (cpu_baseline / --impl reference): the reference package's own numpy path.
 """
 
 from __future__ import annotations
@@ -23,6 +26,7 @@ import numpy as np
 DEFAULT_B = 32
 PROMPT = 128
 CTX = 256
+C3_E, C3_B = 16, 128
 
 
 def _expert_names(E):
@@ -30,56 +34,204 @@ def _expert_names(E):
     return [base[e] if e < 3 else f"expert{e}" for e in range(E)]
 
 
-def build_engine(B, E, seed=0, n_layers=None, device="cuda", experts=None, requests=None):
-    """Engine with the base (replicated) and experts `experts` (global ids; default
-    0..E-1) resident; batch = `requests` (global expert id per request; default
-    round-robin over the resident experts)."""
+def route_requests(domains, B, seed=0, device="cuda"):
+    """Router-assigned batch: B queries (truth round-robin over the domains, shuffled) from
+    disjoint keyword pools, classified by the GPU router.  Returns (expert index per
+    request, router stats)."""
+    import torch
+    from paper_2406_09041_b200 import router as pr
+    rng = np.random.default_rng(seed)
+    pools = {d: [f"{d}{j}" for j in range(12)] for d in domains}
+
+    def query(d):
+        return " ".join(rng.choice(pools[d], size=8))
+
+    r = pr.train_router([(query(d), d) for d in domains for _ in range(16)], domains)
+    dev = pr.DeviceRouter(r, device)
+    truth = [domains[i % len(domains)] for i in range(B)]
+    rng.shuffle(truth)
+    qs = [query(d) for d in truth]
+    # device-resident router forward, CUDA-event timed (the classify of one batch)
+    cps = [np.frombuffer(q.encode("utf-32-le"), dtype="<u4").astype(np.int32) for q in qs]
+    off = np.zeros(B + 1, np.int64)
+    off[1:] = np.cumsum([len(c) for c in cps])
+    d_cps = torch.from_numpy(np.concatenate(cps)).to(device)
+    d_off = torch.from_numpy(off).to(device)
+    for _ in range(3):
+        dev.classify_codepoints(d_cps, d_off)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    reps = 20
+    for _ in range(reps):
+        dom, _, _ = dev.classify_codepoints(d_cps, d_off)
+    en.record()
+    en.synchronize()
+    dev_ms = st.elapsed_time(en) / reps
+    t0 = time.perf_counter()
+    got = dev.classify_batch(qs)  # the public call: host strings -> device -> decisions -> host
+    host_ms = (time.perf_counter() - t0) * 1e3
+    idx = {d: i for i, d in enumerate(domains)}
+    assigned = [idx[name] for name, _, _ in got]
+    acc = float(np.mean([a == idx[t] for a, t in zip(assigned, truth)]))
+    return assigned, {"queries": B, "domains": len(domains), "device_ms_per_batch": dev_ms,
+                      "host_ms_per_batch": host_ms, "accuracy_vs_generator": acc,
+                      "note": "K4 Naive-Bayes n-gram router (SPEC stand-in for the paper's 1.8B LLM router; "
+                              "PAPER.md:560 reports 17.6 ms per 128-token query batch for that model)"}
+
+
+def build_engine(B, experts, requests, max_batch=None, seed=0, n_layers=None, device="cuda"):
+    """Engine with the replicated base (seed `seed`) and experts `experts` (global ids)
+    resident; the batch is `requests` (global expert id per request)."""
     from paper_2406_09041_b200 import compress, synth
     from paper_2406_09041_b200.mistral import MistralMultiExpert
-    experts = list(range(E)) if experts is None else list(experts)
     shape = synth.MistralShape()
-    eng = MistralMultiExpert(shape, max_batch=B + 16 * len(experts), ctx_max=CTX, device=device,
+    eng = MistralMultiExpert(shape, max_batch=max_batch or (B + 16 * len(experts)), ctx_max=CTX, device=device,
                              n_layers=n_layers)
     eng.wrap_positions = True  # steady-state benchmark: long runs wrap positions (never in serving)
     eng.load_synthetic_base(seed=seed)
-    shapes = synth.mistral_expert_shapes(shape, eng.n_layers)
+    add_experts(eng, experts)
+    set_requests(eng, requests)
+    return eng
+
+
+def add_experts(eng, experts):
+    from paper_2406_09041_b200 import compress, synth
+    shapes = synth.mistral_expert_shapes(eng.shape, eng.n_layers)
     names = _expert_names(max(experts) + 1)
     for e in experts:
         blob = synth.synthetic_expert_artifact(1000 + e, shapes, names[e])
         eng.add_expert(names[e], compress.deserialize_artifact(blob))
         del blob
-    if requests is None:
-        requests = [experts[t % len(experts)] for t in range(B)]
-    eng.set_batch([names[e] for e in requests], [PROMPT] * len(requests))
-    eng.fill_random_kv(PROMPT, seed=seed + 7)
-    return eng
 
 
-def run_c2(args, ws, rank, local, ClockSampler, peaks):
+def set_requests(eng, requests, seed=5):
     import torch
-    B = args.batch or DEFAULT_B
-    E = args.experts
-    # expert-sharded weak scaling: E experts per GPU (E*ws in total, expert e on rank e mod ws),
-    # base replicated (seed 0 everywhere); rank 0 assigns B*ws requests round-robin over all
-    # experts and dispatches each to its owner -- a host control message, no data collective
-    from paper_2406_09041_b200.shard import Placement, dispatch
-    pl = Placement(E * ws, ws)
-    reqs = [(i, i % (E * ws), None) for i in range(B * ws)] if rank == 0 else None
-    mine = dispatch(reqs, pl, rank) if ws > 1 else reqs
-    eng = build_engine(B, E, seed=0, experts=pl.local_experts(rank), requests=[r[1] for r in mine])
-    g = torch.Generator(device="cuda")
-    g.manual_seed(5)
-    R = eng.B  # engine rows (expert groups padded to 16-row boundaries)
-    eng.ids[:R] = torch.randint(0, eng.shape.vocab, (R,), generator=g, device="cuda", dtype=torch.int32)
+    names = _expert_names(max(requests) + 1)
+    eng.set_batch([names[e] for e in requests], [PROMPT] * len(requests))
+    eng.fill_random_kv(PROMPT, seed=seed + 2)
+    g = torch.Generator(device=eng.device)
+    g.manual_seed(seed)
+    R = eng.B
+    eng.ids[:R] = torch.randint(0, eng.shape.vocab, (R,), generator=g, device=eng.device, dtype=torch.int32)
+
+
+def _graph_of(plans_fn):
+    import torch
+    g = torch.cuda.CUDAGraph()
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s2):
+        g.capture_begin()
+        n = plans_fn(s2)
+        g.capture_end()
+    torch.cuda.current_stream().wait_stream(s2)
+    return g, n
+
+
+def _time_graph(g, steps, warm=3):
+    import torch
+    for _ in range(warm):
+        g.replay()
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(steps):
+        g.replay()
+    en.record()
+    torch.cuda.synchronize()
+    return st.elapsed_time(en) / steps
+
+
+def linear_decomposition(eng, steps):
+    """Time all fused-linear launches of one decode step (CUDA graph, events on the
+    launching stream): fused (base + deltas), base only, delta only -- the SPEC
+    bench_decode decomposition over the real step."""
+    from paper_2406_09041_b200.device import LinearPlan
+
+    def fused(s):
+        n = 0
+        for (_, _, _, layers, head) in eng._plans:
+            for layer_plans in layers:
+                for p in layer_plans:
+                    p(s)
+                    n += 1
+            head(s)
+            n += 1
+        return n
+
+    def variant(base: bool):
+        plans = []
+        for (_, _, _, layers, head) in eng._plans:
+            for layer_plans in layers:
+                for p in layer_plans:
+                    w, table, out, res = p.keep[1], p.keep[2], p.keep[3], p.keep[4]
+                    a = p.args
+                    segs = [(a.seg_begin[i], a.seg_end[i], a.seg_slot[i]) for i in range(a.n_segments)]
+                    if base:
+                        plans.append(LinearPlan(p.keep[0], a.B, w, None, [], out, residual=res, geom=p.geom,
+                                                num_ctas=a.num_ctas))
+                    elif segs:
+                        plans.append(LinearPlan(p.keep[0], a.B, None, table, segs, out, residual=res, geom=p.geom,
+                                                num_ctas=a.num_ctas, x_corr=p.keep[5]))
+            if base:
+                plans.append(head)
+
+        def run(s):
+            for p in plans:
+                p(s)
+            return len(plans)
+        return run
+
+    g_f, n_lin = _graph_of(fused)
+    t_fused = _time_graph(g_f, steps)
+    g_b, _ = _graph_of(variant(True))
+    t_base = _time_graph(g_b, steps)
+    g_d, n_d = _graph_of(variant(False))
+    t_delta = _time_graph(g_d, steps) if n_d else 0.0
+    return {"fused_ms": t_fused, "base_gemm_ms": t_base, "delta_stage_ms": t_delta, "launches": n_lin}
+
+
+def parity_sample(eng, experts, layers=(0,)):
+    """Sampled-layer parity (outside the timed region): every fused linear of `layers` and
+    the lm_head vs the f64 restatement on the identical bf16 inputs (oracle/parity.py)."""
+    import torch
+    from oracle import mesw as om
+    from oracle.parity import LinearParity
+    from paper_2406_09041_b200 import synth
+    shapes = synth.mistral_expert_shapes(eng.shape, max(layers) + 1)
+    names = _expert_names(max(experts) + 1)
+    blocks = {}
+    for e in experts:
+        _, ls = om.parse_artifact(synth.synthetic_expert_artifact(1000 + e, shapes, names[e]))
+        blocks[names[e]] = ls
+    saved = (eng.ids.clone(), eng.pos.clone(), eng.len.clone())
+    chk = LinearParity(eng, blocks, layers=layers, head=True)
+    eng.step(trace=chk)
+    torch.cuda.synchronize()
+    eng.ids.copy_(saved[0])
+    eng.pos.copy_(saved[1])
+    eng.len.copy_(saved[2])
+    s = chk.summary()
+    return {"max_rel_err": s["max_rel_err"], "argmax_agree": s["argmax_agree"], "tolerance": 1e-2,
+            "linears_checked": s["linears_checked"], "layers": list(layers),
+            "reference": "f64 x.W + delta_matvec (oracle/parity.py) on the identical bf16 inputs",
+            "per_kind": {f"{r['kind']}{'' if r['layer'] < 0 else r['layer']}": r["max_rel_err"]
+                         for r in s["per_linear"]}}
+
+
+def measure_engine(eng, args, ws, local, ClockSampler):
+    """Device-timed decode steps (graph replay), max over ranks."""
+    import torch
     eng.capture()
-    stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         eng.replay()
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
+    stream = torch.cuda.current_stream()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
         st.record(stream)
         for _ in range(args.steps):
             eng.replay()
@@ -89,108 +241,215 @@ def run_c2(args, ws, rank, local, ClockSampler, peaks):
     ms_t = torch.tensor([ms], device="cuda")
     if ws > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(ms_t.item())
+    return float(ms_t.item()), clk.summary()
+
+
+def run_c2(args, ws, rank, local, ClockSampler, peaks):
+    import torch
+    from paper_2406_09041_b200.shard import Placement, ShardedService
+    B = args.batch or DEFAULT_B
+    E = args.experts
+    c5 = getattr(args, "config", "c2") == "c5"
+    pl = Placement(E * ws, ws)
+    # rank 0 routes B*ws queries over all E*ws expert domains and dispatches each request to
+    # its expert's owner (host control message, no data collective)
+    router_stats = None
+    reqs = None
+    if rank == 0:
+        assigned, router_stats = route_requests(_expert_names(E * ws), B * ws, seed=17)
+        reqs = [(i, e, None) for i, e in enumerate(assigned)]
+    mine = []
+
+    def serve_setup(local_reqs):
+        mine.extend(local_reqs)
+        return {}
+
+    ShardedService(pl, rank, serve_setup).step(reqs)
+    extras = ws == 1 and not c5 and not getattr(args, "no_extras", False)
+    eng = build_engine(B, pl.local_experts(rank), [r[1] for r in mine],
+                       max_batch=(C3_B + 16 * C3_E) if extras else None)
+    ms, clocks = measure_engine(eng, args, ws, local, ClockSampler)
     per_step = ms / args.steps
     tok_s = ws * B * args.steps / (ms / 1e3)
     nbytes = eng.bytes_per_step()
 
-    # dominant kernel: the fused multi-expert linear.  Time all linear launches of a step
-    # (4 per layer + lm_head) alone, CUDA events on the launching stream.
-    lin_graph = torch.cuda.CUDAGraph()
-    s2 = torch.cuda.Stream()
-    s2.wait_stream(torch.cuda.current_stream())
-    n_lin = 0
-    with torch.cuda.stream(s2):
-        lin_graph.capture_begin()
-        for (_, _, _, layers, head) in eng._plans:
-            for layer_plans in layers:
-                for p in layer_plans:
-                    p(s2)
-                    n_lin += 1
-            head(s2)
-            n_lin += 1
-        lin_graph.capture_end()
-    torch.cuda.current_stream().wait_stream(s2)
-    for _ in range(3):
-        lin_graph.replay()
-    torch.cuda.synchronize()
-    st.record(stream)
-    for _ in range(args.steps):
-        lin_graph.replay()
-    en.record(stream)
-    torch.cuda.synchronize()
-    lin_ms = st.elapsed_time(en) / args.steps
+    # dominant kernel: all fused-linear launches of a step (+ the SPEC decomposition)
+    dec = linear_decomposition(eng, args.steps)
+    lin_ms = dec["fused_ms"]
     lin_bytes = nbytes["linears"] + nbytes["head"]
     peak, peak_kind = peaks()
     achieved = lin_bytes / (lin_ms / 1e3) / 1e9
-    delta_gbs = nbytes["delta"] / (lin_ms / 1e3) / 1e9 * (nbytes["delta"] / max(nbytes["delta"], 1))
+    base_bytes = nbytes["base_linears"] + nbytes["head"]
+    delta_gbs = nbytes["delta"] / (dec["delta_stage_ms"] / 1e3) / 1e9 if dec["delta_stage_ms"] else None
 
-    # e2e through the public API: pinned host ids -> device -> graph step -> next ids -> host
+    # e2e through the public API, per rank behind the sharded service: pinned host ids ->
+    # device -> graph-replayed step -> next ids -> host, every step
+    R = eng.B
     host_in = torch.zeros(R, dtype=torch.int32).pin_memory()
     host_out = torch.zeros(R, dtype=torch.int32).pin_memory()
     host_in.copy_(eng.ids[:R].cpu())
-    for _ in range(args.warmup):
+
+    svc = ShardedService(pl, rank, make_serve(eng, args.steps, host_in, host_out))
+    for _ in range(max(1, args.warmup // 3)):
         eng.decode(host_in, host_out)
         host_in.copy_(host_out)
+    if ws > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        eng.decode(host_in, host_out)
-        host_in.copy_(host_out)
+    res = svc.step(reqs)
     e2e_s = (time.perf_counter() - t0) / args.steps
     e2e_t = torch.tensor([e2e_s], device="cuda")
     if ws > 1:
         torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
+    if rank == 0:
+        assert res is not None and len(res) == B * ws and all(len(v) == args.steps for v in res.values())
 
-    traffic = None
-    try:
-        import json
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(f"c2_B{B}_E{E}")
-            traffic = tr["traffic"] if tr else None  # dram bytes of one step's linear launches
-    except Exception:
-        pass
-
+    gpus = _gpus_active(ws)
+    traffic = _traffic_of(f"c2_B{B}_E{E}")
     line = {
         "metric": "decode tokens/sec with N mixed experts (Mistral-7B shape); delta-GEMM HBM GB/s",
         "value": tok_s, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init Mistral-7B-shaped base, synthetic 2-bit deltas)",
-        "config": {"workload": (f"c5: 64 experts sharded over {ws} GPU(s), " if getattr(args, "config", "c2") == "c5" else "c2: ")
+        "config": {"workload": (f"c5: {E * ws} experts sharded over {ws} GPU(s), " if c5 else "c2: ")
                                + f"full Mistral-7B decoder stack (32 layers), {E} experts per GPU "
                                f"(b=2 codes + 8 fp16 salient rows on all 224 decoder linears), "
-                               f"batch {B} mixed decode, ctx {PROMPT}+",
-                   "batch": B, "experts": E, "l2": f"per-step weights {nbytes['total']/1e9:.1f} GB >> 126 MB L2",
-                   "parallelism": f"expert-sharded replicas x{ws} (replicated base, no collective)"},
+                               f"batch {B} per GPU router-assigned mixed decode, ctx {PROMPT}+",
+                   "batch": B, "experts": E, "experts_total": E * ws,
+                   "l2": f"per-step weights {nbytes['total']/1e9:.1f} GB >> 126 MB L2",
+                   "parallelism": f"expert-sharded replicas x{ws} (replicated base, expert e on rank e mod {ws}, "
+                                  "router dispatch by host control message, no data collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": f"me_linear_tc_kernel<2, true> (all {n_lin} fused linear launches of a step)",
+                     "kernel": f"me_linear_tc_kernel<2, true> (all {dec['launches']} fused linear launches of a step)",
                      "bytes_per_step": lin_bytes, "kernel_ms_per_step": lin_ms,
                      "kernel_share_of_step": lin_ms / per_step},
-        "delta_gemm": {"bytes_per_step": nbytes["delta"],
-                       "note": "delta bytes (codes+salient+steps) streamed by the fused linears"},
+        "delta_gemm": {"bytes_per_step": nbytes["delta"], "gbs": delta_gbs,
+                       "frac": delta_gbs / peak if delta_gbs else None,
+                       "delta_stage_ms": dec["delta_stage_ms"], "base_gemm_ms": dec["base_gemm_ms"],
+                       "fused_ms": dec["fused_ms"],
+                       "base_gbs": base_bytes / (dec["base_gemm_ms"] / 1e3) / 1e9,
+                       "note": "SPEC bench_decode decomposition over the step's linears: delta-only launches "
+                               "(codes + salient + steps, no base) give the delta-GEMM GB/s"},
         "e2e": {"value": ws * B / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": 4 * R,
-                "d2h_bytes_per_step": 4 * R},
+                "d2h_bytes_per_step": 4 * R,
+                "path": "shard.ShardedService -> MistralMultiExpert.decode (pinned host ids in/out every step)"},
+        "router": router_stats,
         "gpu_launches": eng.launches_per_step() * args.steps,
-        "clocks": clk.summary(),
+        "gpus_active": gpus,
+        "clocks": clocks,
         "step_bytes": nbytes,
     }
-    if rank == 0 and not args.no_cpu_baseline:
-        del eng, lin_graph
+    if extras and rank == 0:
+        line["parity"] = parity_sample(eng, pl.local_experts(rank))
+        line["c3"] = run_c3_leg(eng, args, ClockSampler, local, peaks)
+        del eng
         torch.cuda.empty_cache()
-        cpu = cpu_layer_sample(B, E, reps=1)
-        line["cpu_baseline"] = cpu
+        from bench_impl import c1_leg
+        line["c1"] = c1_leg(args, peaks)
+    else:
+        del eng
+    torch.cuda.empty_cache()
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_layer_sample(B, E, reps=1)
     return line
+
+
+def make_serve(eng, steps, host_in, host_out):
+    """The per-rank `serve` of shard.ShardedService: the rank's requests (already the
+    engine's batch, same order as set_batch got them) decode `steps` tokens through the
+    public API `eng.decode` (pinned host ids in / out every step); returns
+    {request_id: [token, ...]} for the collect step."""
+    def serve(local_reqs):
+        out = {r[0]: [] for r in local_reqs}
+        rows = eng.rows
+        R = eng.B
+        for _ in range(steps):
+            eng.decode(host_in, host_out)
+            host_in.copy_(host_out)
+            for r, q in enumerate(rows[:R]):
+                if q >= 0:
+                    out[local_reqs[q][0]].append(int(host_out[r]))
+        return out
+    return serve
+
+
+def run_c3_leg(eng, args, ClockSampler, local, peaks):
+    """BASELINE config 3 in the same process: the C2 engine (same base) grows to 16 experts,
+    B = 128 router-assigned requests, full 32-layer step."""
+    have = len(eng.experts)
+    add_experts(eng, list(range(have, C3_E)))
+    assigned, rstats = route_requests(_expert_names(C3_E), C3_B, seed=23)
+    set_requests(eng, assigned, seed=9)
+    ms, clocks = measure_engine(eng, args, 1, local, ClockSampler)
+    per_step = ms / args.steps
+    nbytes = eng.bytes_per_step()
+    dec = linear_decomposition(eng, max(3, args.steps // 2))
+    peak, _ = peaks()
+    lin_bytes = nbytes["linears"] + nbytes["head"]
+    achieved = lin_bytes / (dec["fused_ms"] / 1e3) / 1e9
+    delta_gbs = nbytes["delta"] / (dec["delta_stage_ms"] / 1e3) / 1e9 if dec["delta_stage_ms"] else None
+    return {"workload": f"c3: {C3_E} experts on one GPU, batch {C3_B} router-assigned, full 32-layer stack",
+            "value": C3_B * args.steps / (ms / 1e3), "unit": "tokens/s", "ms_per_step": per_step,
+            "launch_groups": len(eng.groups), "rows_padded": eng.B,
+            "roofline": {"achieved": achieved, "peak": peak, "frac": achieved / peak, "unit": "GB/s",
+                         "kernel_ms_per_step": dec["fused_ms"], "bytes_per_step": lin_bytes,
+                         "traffic": _traffic_of(f"c2_B{C3_B}_E{C3_E}")},
+            "delta_gemm": {"gbs": delta_gbs, "frac": delta_gbs / peak if delta_gbs else None,
+                           "delta_stage_ms": dec["delta_stage_ms"], "base_gemm_ms": dec["base_gemm_ms"]},
+            "router": rstats, "clocks": clocks}
+
+
+def _gpus_active(ws):
+    import torch
+    me = torch.cuda.get_device_properties(torch.cuda.current_device())
+    info = {"rank": int(os.environ.get("RANK", "0")), "device": torch.cuda.current_device(),
+            "pci_bus_id": getattr(me, "pci_bus_id", None), "uuid": str(getattr(me, "uuid", ""))}
+    if ws == 1:
+        return {"count": 1, "devices": [info]}
+    allv = [None] * ws
+    torch.distributed.all_gather_object(allv, info)
+    return {"count": len({(d["uuid"], d["pci_bus_id"]) for d in allv}), "devices": allv}
+
+
+def _traffic_of(key):
+    import json
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(key)
+            return tr["traffic"] if tr else None
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------------------- CPU arm
 
-class _CpuLayer:
-    """One Mistral decoder layer on the host, reference-style numpy (f32)."""
+def reference_package():
+    """The unmodified reference package installed by the committed recipe
+    (tools/install_reference.sh -> baseline/_ref, git-ignored, travels to the GPU box), or
+    None (then the oracle port restates the same algorithm)."""
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "meswitch")) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from meswitch import compress as ref_compress  # noqa: F401
+        return ref_compress
+    except Exception:
+        return None
 
-    def __init__(self, B, E, seed=0):
-        from oracle import mesw as om
-        from paper_2406_09041_b200 import compress, synth
+
+class _CpuLayer:
+    """One Mistral decoder layer on the host, the reference's numpy path (f32): the shared-base
+    x@W for the batch, then per expert group x_g @ CompressedDelta.reconstruct() -- with the
+    reference's OWN deserialize_artifact / reconstruct (compress.py:115-121, :513-549) when the
+    package is installed, else the oracle port -- plus RMSNorm / RoPE / attention / SwiGLU."""
+
+    PROJ = ("q", "k", "v", "o", "gate", "up", "down")
+
+    def __init__(self, B, E, seed=0, groups=None):
+        from paper_2406_09041_b200 import synth
         self.shape = s = synth.MistralShape()
         rng = np.random.default_rng(seed)
         kv = s.n_kv_heads * s.head_dim
@@ -199,18 +458,24 @@ class _CpuLayer:
                      "down": (s.intermediate, s.hidden)}
         self.W = {n: (rng.standard_normal(size=d, dtype=np.float32) * 0.02) for n, d in self.dims.items()}
         self.norm = np.ones(s.hidden, np.float32)
-        shapes = [self.dims[n] for n in ("q", "k", "v", "o", "gate", "up", "down")]
-        self.layers = []  # per expert: dict proj -> oracle layer
+        shapes = [self.dims[n] for n in self.PROJ]
+        ref = reference_package()
+        self.kind = "reference" if ref is not None else "port"
+        self.layers = []  # per expert: dict proj -> layer object with .reconstruct()
         for e in range(E):
             blob = synth.synthetic_expert_artifact(1000 + e, shapes, f"e{e}")
-            _, ls = om.parse_artifact(blob)
-            self.layers.append(dict(zip(("q", "k", "v", "o", "gate", "up", "down"), ls)))
+            if ref is not None:
+                ls = ref.deserialize_artifact(blob).layers  # the reference's own parser
+            else:
+                from oracle import mesw as om
+                _, ls = om.parse_artifact(blob)
+            self.layers.append(dict(zip(self.PROJ, ls)))
         self.dense = None
         self.B, self.E = B, E
         self.kc = rng.standard_normal(size=(B, PROMPT + 1, s.n_kv_heads, s.head_dim), dtype=np.float32)
         self.vc = rng.standard_normal(size=(B, PROMPT + 1, s.n_kv_heads, s.head_dim), dtype=np.float32)
         self.h = rng.standard_normal(size=(B, s.hidden), dtype=np.float32)
-        self.groups = [np.arange(B)[np.arange(B) % E == e] for e in range(E)]
+        self.groups = groups if groups is not None else [np.arange(B)[np.arange(B) % E == e] for e in range(E)]
 
     def cache_dense(self):
         self.dense = [{n: L.reconstruct() for n, L in per.items()} for per in self.layers]
@@ -279,22 +544,28 @@ def cpu_layer_sample(B, E, reps=1):
         layer.step()
     t_layer = (time.perf_counter() - t0) / reps
     t_step = 32 * t_layer + _head_time(B)
-    return {"value": B / t_step, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{reps} x one decoder layer (7 projections, B={B}, {E} experts, dense deltas cached = "
-                      f"reference best case) timed, scaled x32 layers + lm_head; numpy/OpenBLAS all threads",
+    return {"value": B / t_step, "unit": "tokens/s", "cores": os.cpu_count(), "kind": layer.kind,
+            "sample": f"{reps} x one decoder layer (7 projections, B={B}, {E} experts, dense deltas cached by the "
+                      f"{'reference package' if layer.kind == 'reference' else 'oracle port'}'s reconstruct() = "
+                      f"its best case) timed, scaled x32 layers + lm_head; numpy/OpenBLAS all threads",
             "layer_s": t_layer}
 
 
-def _time_layer(layer, steps, warmup):
+def _time_layer(layer, steps, warmup, cached=True):
     for _ in range(warmup):
-        layer.step()
+        layer.step(cached)
     t0 = time.perf_counter()
     for _ in range(steps):
-        layer.step()
+        layer.step(cached)
     return (time.perf_counter() - t0) / steps
 
 
 def reference_arm_c2(args):
+    """--impl reference for c2/c5: each timed step is a bounded sample of the decode step --
+    ONE of the 32 decoder layers (7 projections, all experts of the batch, glue) -- run by
+    the reference package's own numpy path (reconstruct() cached per expert = its best case).
+    `ms_per_step` is that real timed step; `value` scales it to the full stack (x32 layers +
+    lm_head).  The as-shipped variant (reconstruct() on every call) is timed once beside it."""
     ws = args.gpus
     c5 = getattr(args, "config", "c2") == "c5"
     if c5:  # the rank-0 share of 64 sharded experts, batch 128 per GPU (as the GPU arm)
@@ -307,8 +578,11 @@ def reference_arm_c2(args):
     E_s = min(E, 4)
     layer = _CpuLayer(B, E_s)
     layer.cache_dense()
+    t0 = time.perf_counter()
     t_layer = _time_layer(layer, args.steps, args.warmup)
-    sample = f"each step = one decoder layer (B={B}, {E} experts, cached dense deltas) scaled x32 + lm_head"
+    timed_s = time.perf_counter() - t0
+    sample = (f"each step = one of the 32 decoder layers (B={B}, {E} experts, 7 projections + glue, dense deltas "
+              f"cached), value scaled x32 + lm_head")
     if E_s < E:
         groups, layer.groups = layer.groups, []
         t_base = _time_layer(layer, args.steps, 1)
@@ -318,15 +592,25 @@ def reference_arm_c2(args):
                   f"(cached dense deltas) and scaled x{E / E_s:g}; x32 layers + lm_head")
     t_step = 32 * t_layer + _head_time(B)
     val = B / t_step
+    # as shipped: every call re-decodes the packed codes (reconstruct() per projection per group)
+    t_ship = _time_layer(layer, 1, 0, cached=False)
+    if E_s < E:
+        t_ship = t_base + (E / E_s) * (t_ship - t_base)
+    ship_val = B / (32 * t_ship + _head_time(B))
+    kind = layer.kind
     return {"impl": "reference", "metric": "decode tokens/sec with N mixed experts (Mistral-7B shape); "
                                           "delta-GEMM HBM GB/s",
             "value": val, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": t_layer * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": (f"c5: 64 experts sharded over {ws} GPU(s), " if getattr(args, "config", "c2") == "c5" else "c2: ")
-                               + f"full Mistral-7B decoder stack (32 layers), {E} experts per GPU "
+            "config": {"workload": (f"c5: 64 experts sharded over {ws} GPU(s), " if c5 else "c2: ")
+                                   + f"full Mistral-7B decoder stack (32 layers), {E} experts per GPU "
                                    f"(b=2 codes + 8 fp16 salient rows on all 224 decoder linears), "
                                    f"batch {B} mixed decode, ctx {PROMPT}+", "batch": B, "experts": E},
-            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "timed_region_s": timed_s,
+            "ms_per_full_step_scaled": t_step * 1e3,
+            "as_shipped": {"value": ship_val, "unit": "tokens/s", "layer_s": t_ship,
+                           "note": "reconstruct() on every call (the reference has no fused kernel)"},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": os.cpu_count(), "kind": kind,
                              "sample": sample},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

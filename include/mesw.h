@@ -302,7 +302,7 @@ int mesw_quantize_pack(const float* d_delta, uint32_t m, uint32_t n, const float
  * hashing and f64 summation order as pinned in oracle/router.py.
  *   d_codepoints  int32 Unicode code points of all queries, concatenated
  *   d_offsets     int64[B+1]: query q = code points [off[q], off[q+1])
- *   d_loglik      f32[D][65536], d_logprior f32[D], 1 <= D <= 32 (one warp lane per domain)
+ *   d_loglik      f32[D][65536], d_logprior f32[D], 1 <= D <= 64 (two domains per warp lane)
  * Outputs: d_domain[B] (argmax, ties -> lowest id), d_conf[B] (softmax of the
  * winner), d_prior_only[B] (1 when the query has no n-gram; may be NULL).      */
 int mesw_router_classify(const int32_t* d_codepoints, const int64_t* d_offsets, int B,

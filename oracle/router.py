@@ -29,7 +29,7 @@ import numpy as np
 N_BUCKETS = 1 << 16
 FNV_OFFSET = 2166136261
 FNV_PRIME = 16777619
-MAX_DOMAINS = 32  # one warp lane per domain in K4; render_prompt alone caps at 6
+MAX_DOMAINS = 64  # two domains per warp lane in K4; render_prompt alone caps at 6
 
 
 def fnv1a32(data: bytes) -> int:

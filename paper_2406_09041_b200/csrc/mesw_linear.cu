@@ -42,8 +42,17 @@ constexpr int kMaxIssuers = 3;  // warps 1..3
 constexpr int kDqWarp0 = 4, kEpiWarp0 = kDqWarp0 + 4 * kDqGroups;
 constexpr int kThreads = (kEpiWarp0 + 4) * 32;  // 16 warps
 constexpr int kTmemCols = 512;
-constexpr int kMaxASlots = 8;
-constexpr int kAColsPerSlot = 64;  // one job's A tile (128 x 128 bf16) per slot
+#ifndef MESW_HALF_JOBS
+#define MESW_HALF_JOBS 1
+#endif
+// A job = one expert's dequantised A tile for one unit: 128 outputs x 128 k (64 TMEM columns),
+// or, with half jobs (default), each k-half (128 x 64, 32 columns) is its own job with its own
+// slot, so a dequant group fills one half-slot while the tensor pipe still reads the other
+// (at many experts per launch the TMEM budget leaves one full slot per issuer, and a single
+// slot serialises dequant -> issue -> MMA -> slot free).
+constexpr int kJobHalves = MESW_HALF_JOBS ? 2 : 1;
+constexpr int kMaxASlots = 16;
+constexpr int kAColsPerSlot = 64 / kJobHalves;
 constexpr int kMaxRows = 192;  // padded token rows per launch (TMEM: 2 * rows <= 384)
 constexpr int kMaxStages = 8;
 constexpr int kMaxCStages = 16;
@@ -216,6 +225,12 @@ __device__ __forceinline__ void mma2_ts_k128(uint32_t d, uint32_t a_tmem, uint64
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
       MESW_TS_STEP(1) MESW_TS_STEP(2) MESW_TS_STEP(3) MESW_TS_STEP(4) MESW_TS_STEP(5) MESW_TS_STEP(6)
       MESW_TS_STEP(7) "}\n" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma2_ts_k64(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b32 at;\n.reg .b64 bd;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      MESW_TS_STEP(1) MESW_TS_STEP(2) MESW_TS_STEP(3) "}\n" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 #undef MESW_TS_STEP
 
@@ -601,9 +616,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // Cycle-count profiling of the role loops (tools/ktiming.py): compiled in only with
 // -DMESW_PROFILE (MESW_PROFILE=1 python build.py --force); zero cost otherwise.
-#ifndef MESW_EXP_KH
-#define MESW_EXP_KH 2  // experiment switch: k-halves dequantized per job (2 = correct)
-#endif
 #ifdef MESW_PROFILE
 #define MESW_PROF(...) __VA_ARGS__
 #else
@@ -824,7 +836,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           }
           // this issuer's segments: seg_issuer() is round-robin, so stride through them
           for (int q = q_own0; q < p.n_seg; q += q_step) {
-            {
+#pragma unroll 1
+            for (int kh = 0; kh < kJobHalves; ++kh) {
               MESW_PROF(tq = clock64();)
               mbar_wait_cluster(&S.afull[abase_own + aslot], aph);
               MESW_PROF(prof[3] += clock64() - tq;)
@@ -836,9 +849,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               const uint32_t dd = d_base + (uint32_t)(NP + win0);
               const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + (abase_own + aslot) * kAColsPerSlot);
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
-              const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4));
+              const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4)) + (uint64_t)(kh * 64);
 #ifndef MESW_EXP_NOMMA
-              mma2_ts_k128(uni(dd), uni(a0), uni64(bd), uni(id), uni(f0));
+              if (kJobHalves == 2) mma2_ts_k64(uni(dd), uni(a0), uni64(bd), uni(id), uni(kh == 0 ? f0 : 1u));
+              else mma2_ts_k128(uni(dd), uni(a0), uni64(bd), uni(id), uni(f0));
 #endif
               tc2_commit_w(&S.aempty[abase_own + aslot]);
               if (++aslot == na_own) { aslot = 0; aph ^= 1; }
@@ -897,16 +911,19 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             mbar_wait(&S.cfull[sc], pc);
             MESW_PROF(dprof[0] += clock64() - dq;)
             const uint8_t* cst = ring + p.co + (size_t)sc * p.cbytes;
-            for (int q = sg0 + ((grp - sg0 % n_dq) + n_dq) % n_dq; q < sg1; q += n_dq) {
+            for (int q = sg0 + ((grp - sg0 % n_dq) + n_dq) % n_dq; q < sg1; q += n_dq)
+#pragma unroll 1
+            for (int jh = 0; jh < kJobHalves; ++jh) {
               const int aslot = ab + pos;
-              uint32_t cw[2 * WPK];
+              constexpr int KH = 2 / kJobHalves;  // k-halves per job
+              uint32_t cw[KH * WPK];
               const uint8_t* cb = cst + (size_t)(q - sg0) * CB;
 #pragma unroll
-              for (int kh = 0; kh < 2; ++kh)
+              for (int kk = 0; kk < KH; ++kk)
 #pragma unroll
                 for (int v = 0; v < CHB / 16; ++v) {
-                  const uint4 t4 = lds128(cb + ((size_t)kh * 128 + mrow) * CHB + v * 16);
-                  const int w0 = kh * WPK + 4 * v;
+                  const uint4 t4 = lds128(cb + ((size_t)(jh * KH + kk) * 128 + mrow) * CHB + v * 16);
+                  const int w0 = kk * WPK + 4 * v;
                   cw[w0] = t4.x; cw[w0 + 1] = t4.y; cw[w0 + 2] = t4.z; cw[w0 + 3] = t4.w;
                 }
               MESW_PROF(const bool jst = p.tbuf && blockIdx.x == 0 && threadIdx.x == kDqWarp0 * 32 + grp * 128 && dprof[7] < 32;)
@@ -919,11 +936,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + aslot * kAColsPerSlot);
 #ifndef MESW_EXP_NODQ
 #pragma unroll
-              for (int kh = 0; kh < MESW_EXP_KH; ++kh) {
+              for (int kk = 0; kk < KH; ++kk) {
                 uint32_t r[32];
-                if (OFF) dequant_chunk2_offset(&cw[kh * WPK], r);
-                else dequant_chunk<DB>(&cw[kh * WPK], r);
-                tmem_st32(a0 + lane_addr + 32 * kh, r);
+                if (OFF) dequant_chunk2_offset(&cw[kk * WPK], r);
+                else dequant_chunk<DB>(&cw[kk * WPK], r);
+                tmem_st32(a0 + lane_addr + 32 * kk, r);
               }
 #endif
               MESW_PROF(dprof[2] += clock64() - dq;)

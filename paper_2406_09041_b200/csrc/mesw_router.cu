@@ -3,10 +3,10 @@
 //
 // One warp per query.  The warp walks the query's n-grams (all 2-grams, then all 3-grams)
 // 32 at a time: lane j hashes n-gram j (FNV-1a over its UTF-8 bytes, low 16 bits), then
-// the buckets are broadcast in order and lane d (< D domains) accumulates
-// f64(loglik[d][bucket]) sequentially -- the same additions, in the same order, as the
+// the buckets are broadcast in order and lane d accumulates f64(loglik[d][bucket]) (and
+// domain d + 32's, D <= 64) sequentially -- the same additions, in the same order, as the
 // CPU restatement, so the argmax (ties -> lowest id) is bit-identical.  The tables
-// (D x 2^16 f32, <= 1.5 MiB) stay L2-resident across queries.
+// (D x 2^16 f32, 256 KiB per domain) stay L2-resident across queries.
 
 #include <math.h>
 
@@ -16,7 +16,7 @@
 namespace mesw {
 
 constexpr int kRouterBuckets = 1 << 16;
-constexpr int kRouterMaxDomains = 32;  // one lane per domain
+constexpr int kRouterMaxDomains = 64;  // two domains per lane
 constexpr int kRouterWarps = 4;  // queries per block
 
 __device__ __forceinline__ uint32_t fnv_byte(uint32_t h, uint32_t b) { return (h ^ b) * 16777619u; }
@@ -45,8 +45,12 @@ __global__ void __launch_bounds__(kRouterWarps * 32) router_classify_kernel(
   const int L = (int)(offsets[qi + 1] - c0);
   const int n2 = L >= 2 ? L - 1 : 0, n3 = L >= 3 ? L - 2 : 0;
   const int G = n2 + n3;
-  const float* row = loglik + (size_t)(lane < D ? lane : 0) * kRouterBuckets;
-  double s = lane < D ? (double)logprior[lane] : 0.0;
+  // lane owns domains d0 = lane and d1 = lane + 32 (D <= 64); each summed sequentially in f64
+  const int d0 = lane, d1 = lane + 32;
+  const float* row0 = loglik + (size_t)(d0 < D ? d0 : 0) * kRouterBuckets;
+  const float* row1 = loglik + (size_t)(d1 < D ? d1 : 0) * kRouterBuckets;
+  double s0 = d0 < D ? (double)logprior[d0] : 0.0;
+  double s1 = d1 < D ? (double)logprior[d1] : 0.0;
   for (int g0 = 0; g0 < G; g0 += 32) {
     const int g = g0 + lane;
     uint32_t bucket = 0;
@@ -59,25 +63,36 @@ __global__ void __launch_bounds__(kRouterWarps * 32) router_classify_kernel(
     }
     const int cnt = min(32, G - g0);
     // gather this lane's 32 terms first (independent loads), then add them in order
-    float v[32];
+    float v0[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const uint32_t b = __shfl_sync(0xffffffffu, bucket, j);
-      v[j] = (j < cnt && lane < D) ? __ldg(row + b) : 0.f;
+      v0[j] = (j < cnt && d0 < D) ? __ldg(row0 + b) : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (j < cnt) s += (double)v[j];
+      if (j < cnt) s0 += (double)v0[j];
+    if (D > 32) {  // warp-uniform
+      float v1[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t b = __shfl_sync(0xffffffffu, bucket, j);
+        v1[j] = (j < cnt && d1 < D) ? __ldg(row1 + b) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < cnt) s1 += (double)v1[j];
+    }
   }
-  // argmax over lanes 0..D-1 (ties -> lowest id), then softmax of the winner
-  double best = s;
-  int win = lane;
+  // argmax over domains 0..D-1 in id order (ties -> lowest id), then softmax of the winner
+  double best = 0.0;
+  int win = 0;
   for (int d = 0; d < D; ++d) {
-    const double sd = __shfl_sync(0xffffffffu, s, d);
+    const double sd = __shfl_sync(0xffffffffu, d < 32 ? s0 : s1, d & 31);
     if (d == 0 || sd > best) { best = sd; win = d; }
   }
   double z = 0.0;
-  for (int d = 0; d < D; ++d) z += exp(__shfl_sync(0xffffffffu, s, d) - best);
+  for (int d = 0; d < D; ++d) z += exp(__shfl_sync(0xffffffffu, d < 32 ? s0 : s1, d & 31) - best);
   if (lane == 0) {
     out_domain[qi] = win;
     out_conf[qi] = (float)(1.0 / z);
@@ -92,7 +107,7 @@ using namespace mesw;
 extern "C" int mesw_router_classify(const int32_t* d_codepoints, const int64_t* d_offsets, int B,
                                     const float* d_loglik, const float* d_logprior, int D, int32_t* d_domain,
                                     float* d_conf, int32_t* d_prior_only, void* stream) {
-  if (B < 0 || D < 1 || D > kRouterMaxDomains) return mesw_fail(MESW_ERR_VALUE, "router: 1..32 domains");
+  if (B < 0 || D < 1 || D > kRouterMaxDomains) return mesw_fail(MESW_ERR_VALUE, "router: 1..64 domains");
   if (!d_offsets || !d_loglik || !d_logprior || !d_domain || !d_conf)
     return mesw_fail(MESW_ERR_VALUE, "router: null buffer");
   if (B == 0) return MESW_OK;

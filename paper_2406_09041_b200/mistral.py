@@ -115,7 +115,9 @@ class MistralMultiExpert:
         # (the fused linears' inputs live in per-launch-group canonical buffers: _build_plans)
         self.qkv = torch.zeros((B, self.g_qkv.n_pad), dtype=bf, device=dev)
         self.gu = torch.zeros((B, self.g_gu.n_pad), dtype=bf, device=dev)
-        self.logits = torch.zeros((B, self.g_head.n_pad), dtype=bf, device=dev)
+        # f32 logits: greedy argmax over bf16-rounded logits would tie / misorder near-equal
+        # candidates (a 32000-way argmax; the f32 epilogue value is what the reference compares)
+        self.logits = torch.zeros((B, self.g_head.n_pad), dtype=torch.float32, device=dev)
         kv_shape = (self.n_layers, B, self.ctx_max, s.n_kv_heads, s.head_dim)
         self.kcache = torch.zeros(kv_shape, dtype=bf, device=dev)
         self.attn_ws = torch.empty(int(_lib.lib().mesw_attention_workspace_bytes(B, s.n_heads, self.ctx_max)),
@@ -486,7 +488,7 @@ class MistralMultiExpert:
             head(stream)
             if trace:
                 trace("post", "head", -1, r0, r1, bufs)
-        chk(L.mesw_argmax(self.logits.data_ptr(), 1, B, s.vocab, self.logits.stride(0), self.ids.data_ptr(), st))
+        chk(L.mesw_argmax(self.logits.data_ptr(), 0, B, s.vocab, self.logits.stride(0), self.ids.data_ptr(), st))
         wrap_to = min(self.ctx_max - 1, 128) if self.wrap_positions else -1
         chk(L.mesw_advance_positions(self.pos.data_ptr(), self.len.data_ptr(), B, self.ctx_max, wrap_to, st))
 
@@ -538,15 +540,19 @@ class MistralMultiExpert:
         n_exp = len(self.segments)
         lin = 0
         delta = 0
+        base = 0
         for g in (self.g_qkv, self.g_o, self.g_gu, self.g_down):
             lin += linear_bytes(g.m, g.n, n_exp, B)
             delta += linear_bytes(g.m, g.n, n_exp, B, base=False) - 2 * B * (g.m + g.n)
+            base += linear_bytes(g.m, g.n, 0, B)
         lin *= self.n_layers
         delta *= self.n_layers
+        base *= self.n_layers
         head = linear_bytes(s.hidden, s.vocab, 0, B)
         ctx = int(self.len[:B].float().mean().item())
         kv = 2 * B * ctx * s.n_kv_heads * s.head_dim * 2 * self.n_layers
-        return {"linears": lin, "delta": delta, "head": head, "kv": kv, "total": lin + head + kv}
+        return {"linears": lin, "delta": delta, "base_linears": base, "head": head, "kv": kv,
+                "total": lin + head + kv}
 
     # ------------------------------------------------------------------ public API
     def decode(self, host_ids: torch.Tensor, out_host: torch.Tensor | None = None) -> torch.Tensor:

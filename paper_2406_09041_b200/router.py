@@ -21,7 +21,7 @@ __all__ = ["Router", "train_router", "save_router", "load_router", "DeviceRouter
            "classify_batch", "evaluate_router", "render_prompt", "ngram_buckets", "N_BUCKETS"]
 
 N_BUCKETS = 1 << 16
-MAX_DOMAINS = 32  # classification: one warp lane per domain (K4); the prompt template caps at 6
+MAX_DOMAINS = 64  # classification: two domains per warp lane (K4); the prompt template caps at 6
 PROMPT_MAX_OPTIONS = 6  # render_prompt enumerates A..F
 MERT_MAGIC = b"MERT"
 MERT_VERSION = 1

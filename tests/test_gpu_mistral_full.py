@@ -9,7 +9,7 @@ router-assigned experts and the serving engine's offset-code path.
   windows when the row budget allows it, else launch groups.
 
 Tolerance (north_star): max rel err <= 1e-2 per linear; logits argmax agreement reported
-and required >= 0.95 (first-maximum argmax over bf16 logits vs f64 logits).
+and required >= 0.97 (first-maximum argmax over the engine's f32 logits vs f64 logits).
 """
 
 import os
@@ -41,8 +41,7 @@ def _router_batch(domains, B, seed):
     truth = [domains[i % len(domains)] for i in range(B)]
     rng.shuffle(truth)
     qs = [query(d) for d in truth]
-    got = dev.classify_batch(qs)
-    picked = [domains[int(d)] for d in got[0]]
+    picked = [name for name, _, _ in dev.classify_batch(qs)]
     assert picked == truth  # separable pools: the router recovers every domain
     return picked
 
@@ -89,7 +88,7 @@ def test_mistral_dims_per_linear_parity(n_layers, n_experts, B, layers):
     assert kinds == {(k, l) for l in layers for k in ("qkv", "o", "gu", "down")} | {("head", -1)}
     bad = [r for r in s["per_linear"] if not r["max_rel_err"] <= TOL]
     assert not bad, bad
-    assert s["argmax_agree"] >= 0.95, s["argmax_agree"]
+    assert s["argmax_agree"] >= 0.97, s["argmax_agree"]
     print(f"\n{n_experts} experts, B={B}: max rel err {s['max_rel_err']:.2e} over {s['linears_checked']} "
           f"launches, argmax agreement {s['argmax_agree']:.3f}")
 

@@ -50,3 +50,25 @@ def test_router_gpu_accuracy_and_evaluate():
     ev = pr.evaluate_router(r, make_records(25, seed=8))
     assert ev["accuracy"] == 1.0
     assert ev["confusion"].sum(axis=1).tolist() == [25] * 4
+
+
+@pytest.mark.parametrize("D", [16, 33, 64])
+def test_router_gpu_many_domains_match_oracle(D):
+    """C3/C5 routing: 16 and 64 expert domains (two per warp lane past 32), decisions and
+    confidences equal to the restatement; synthetic keyword pools are separable."""
+    from paper_2406_09041_b200 import router as pr
+    rng = np.random.default_rng(D)
+    doms = tuple(f"dom{i}" for i in range(D))
+    pools = {d: [f"{d}w{j}" for j in range(10)] for d in doms}
+    rec = [(" ".join(rng.choice(pools[d], size=5)), d) for d in doms for _ in range(8)]
+    r = pr.train_router(rec, doms)
+    o = orc.OracleRouter(r.domains, r.logprior, r.loglik)
+    qs = [" ".join(rng.choice(pools[d], size=4)) for d in doms] + _queries(D, 60)
+    got = pr.DeviceRouter(r).classify_batch(qs)
+    for i, (q, (name, conf, flag)) in enumerate(zip(qs, got)):
+        d, c, f = orc.classify(o, q)
+        assert name == r.domains[d], q
+        assert flag == f
+        assert abs(conf - c) <= 1e-6 * max(1.0, abs(c))
+        if i < D:
+            assert name == doms[i]

@@ -115,3 +115,27 @@ def test_base_digest_matches_reference_manifests():
     with open(os.path.join(GOLDEN, "toy_expert_0.mesw"), "rb") as f:
         man, _ = om.parse_artifact(f.read())
     assert base_digest(mats) == man["base_digest"]
+
+
+def test_mistral_shape_reference_block():
+    """The k_proj-shaped block made by the reference's compress_layer (make_mistral_golden.py):
+    the oracle parses it and its reconstruct() hashes to the reference's own; x @ recon matches."""
+    import hashlib
+    import json
+    with open(os.path.join(GOLDEN, "kat_mistral.json")) as f:
+        kat = json.load(f)
+    _, (L,) = om.parse_artifact(_read(kat["file"]))
+    assert (L.m, L.n, L.bits, L.k) == (kat["m"], kat["n"], kat["bits"], kat["k"])
+    assert L.salient_idx.tolist() == kat["salient"]
+    recon = L.reconstruct()
+    assert hashlib.sha256(np.ascontiguousarray(recon, "<f4").tobytes()).hexdigest() == kat["recon_sha256"]
+    x = np.random.default_rng(7).normal(0, 1, size=(4, L.m)).astype(np.float32)
+    np.testing.assert_allclose(om.delta_matvec_batch(x, L), np.load(os.path.join(GOLDEN, "ref_kproj_y.npy")),
+                               rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("m", [4, 7, 200, 4096])
+def test_vectorised_2bit_unpack_equals_window_decode(m):
+    rng = np.random.default_rng(m)
+    L = om.random_layer(rng, m, 37, 2, min(3, m))
+    assert np.array_equal(L.codes(), L.unpack_generic())

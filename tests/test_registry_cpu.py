@@ -146,3 +146,49 @@ def test_from_root(tmp_path):
     (tmp_path / "registry.json").write_text(json.dumps(man))
     reg = ExpertRegistry.from_root(str(tmp_path), 10 * _size(blobs["math"]), loader=lambda e, a: e)
     assert reg.acquire("code") == "code"
+
+
+def test_eviction_waits_for_release_fence_and_size_fn():
+    """release(eid, stream) records the consumer fence on the handle; eviction calls
+    wait_idle() on the victim BEFORE the unloader frees it; size_fn sets the budget unit."""
+    events = []
+
+    class H:
+        def __init__(self, eid):
+            self.eid = eid
+
+        def fence(self, stream=None):
+            events.append(("fence", self.eid, stream))
+
+        def wait_idle(self):
+            events.append(("wait", self.eid))
+
+    blobs = {e: _blob(i) for i, e in enumerate("ABC")}
+    reg = ExpertRegistry(2000, "synthetic", loader=lambda e, a: H(e),
+                         unloader=lambda e, h: events.append(("unload", e)), size_fn=lambda art: 1000)
+    for e, b in blobs.items():
+        assert reg.register(e, b).size_bytes == 1000
+    reg.acquire("A")
+    reg.release("A", "decode-stream")
+    reg.acquire("B")
+    reg.release("B", "decode-stream")
+    reg.acquire("C")  # evicts A (LRU)
+    assert events[:2] == [("fence", "A", "decode-stream"), ("fence", "B", "decode-stream")]
+    assert events[2:] == [("wait", "A"), ("unload", "A")]
+    assert reg.stats().current_bytes == 2000
+
+
+def test_salient_index_out_of_range_rejected():
+    """An artifact whose salient index is >= rows loads nowhere (the reference's reconstruct()
+    raises IndexError, compress.py:119-120): the C ABI table builder rejects it."""
+    import ctypes as C
+    from paper_2406_09041_b200 import _lib
+    from paper_2406_09041_b200.device import LinearGeometry, build_salient_tables
+    from oracle import mesw as om
+    rng = np.random.default_rng(0)
+    ol = om.random_layer(rng, 64, 128, 2, 3)
+    ol.salient_idx = np.array([5, 9, 64])  # 64 == rows: out of range
+    art = compress.deserialize_artifact(om.serialize_artifact(
+        {"model_id": "x", "domain": "d", "base_digest": "0", "layer_count": 1}, [ol]))
+    with pytest.raises(IndexError):
+        build_salient_tables(art.layers, LinearGeometry(64, (128,)))

@@ -59,7 +59,7 @@ def test_train_errors():
     with pytest.raises(ValueError):
         pr.train_router([("x", "nope")], ("code",))
     with pytest.raises(ValueError):
-        pr.Router(tuple(f"d{i}" for i in range(33)), np.zeros(33, np.float32), np.zeros((33, pr.N_BUCKETS), np.float32))
+        pr.Router(tuple(f"d{i}" for i in range(65)), np.zeros(65, np.float32), np.zeros((65, pr.N_BUCKETS), np.float32))
 
 
 def test_mert_roundtrip_and_errors():

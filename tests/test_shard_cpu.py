@@ -105,3 +105,86 @@ def test_sharded_service_gloo_world2():
     ref = _serve_oracle(W, layers)(reqs)
     for rid, v in results.items():
         assert np.array_equal(np.asarray(v), np.asarray(ref[rid]))
+
+
+class _FakeEngine:
+    """CPU stand-in with the serving engine's batch contract (MistralMultiExpert.set_batch:
+    requests regrouped by expert on 16-row boundaries, rows[r] = request index or -1;
+    decode(host_in, host_out) -> next ids).  Next id = f(expert, current id): a pure
+    function, so the collected token streams are checkable per request."""
+
+    def __init__(self, experts):
+        self.slot = {e: i for i, e in enumerate(experts)}
+
+    def set_batch(self, expert_ids, prompt_lens=None):
+        rows = []
+        for e in sorted(set(expert_ids), key=lambda e: self.slot[e]):
+            while len(rows) % 16:
+                rows.append(-1)
+            rows.extend(i for i, x in enumerate(expert_ids) if x == e)
+        self.rows = np.asarray(rows)
+        self.B = len(rows)
+        self.exp = [expert_ids[q] if q >= 0 else None for q in rows]
+        return self.rows
+
+    def decode(self, host_in, host_out):
+        for r in range(self.B):
+            e = self.exp[r]
+            host_out[r] = 0 if e is None else (int(host_in[r]) * 7 + 13 * e + 1) % 1000
+        return host_out
+
+
+def _expected_stream(e, tok0, steps):
+    out, t = [], tok0
+    for _ in range(steps):
+        t = (t * 7 + 13 * e + 1) % 1000
+        out.append(t)
+    return out
+
+
+def _engine_worker(rank, ws, port, q):
+    import torch
+    import torch.distributed as dist
+    import bench_mistral as bm
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=ws)
+    try:
+        n_exp, steps = 6, 4
+        pl = Placement(n_exp, ws)
+        reqs = [(100 + i, (3 * i + 1) % n_exp, None) for i in range(19)] if rank == 0 else None
+        mine = []
+        ShardedService(pl, rank, lambda lr: (mine.extend(lr), {})[1]).step(reqs)
+        eng = _FakeEngine(pl.local_experts(rank))
+        eng.set_batch([r[1] for r in mine])
+        host_in = torch.zeros(max(eng.B, 1), dtype=torch.int32)
+        for r, qi in enumerate(eng.rows):
+            host_in[r] = 0 if qi < 0 else mine[qi][0]  # first token = request id
+        host_out = torch.zeros_like(host_in)
+        res = ShardedService(pl, rank, bm.make_serve(eng, steps, host_in, host_out)).step(reqs)
+        if rank == 0:
+            q.put(("res", res))
+        q.put(("mine", rank, [r[0] for r in mine]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_engine_serve_path_world_size_2():
+    """bench_mistral.make_serve (the per-rank serve the benchmark's e2e runs) behind
+    ShardedService over gloo: every request decoded on its owner rank, token streams
+    returned to rank 0 in request order, none lost or duplicated."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_engine_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(3)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res = next(g[1] for g in got if g[0] == "res")
+    mine = {g[1]: g[2] for g in got if g[0] == "mine"}
+    assert sorted(mine[0] + mine[1]) == [100 + i for i in range(19)]
+    for i in range(19):
+        e = (3 * i + 1) % 6
+        assert (100 + i) in mine[e % 2]
+        assert res[100 + i] == _expected_stream(e, 100 + i, 4)

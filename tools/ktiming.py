@@ -17,7 +17,8 @@ x = torch.randn((rows, m), device="cuda").to(torch.bfloat16)
 y = torch.empty((rows, n), dtype=torch.bfloat16, device="cuda")
 corr = corr_table(rows, m, "cuda") if os.environ.get("EXACT") is None else None
 xc = pack_x(x, corr=corr)
-plans = [LinearPlan(xc, rows, dw, table if E else None, segs, y, geom=geom, x_corr=corr) for geom, dw, table in sets]
+nobase = os.environ.get("NOBASE") is not None  # delta-only launches (no base weight)
+plans = [LinearPlan(xc, rows, None if nobase else dw, table if E else None, segs, y, geom=geom, x_corr=corr) for geom, dw, table in sets]
 for i in range(6): plans[i % 3]()
 torch.cuda.synchronize()
 plans[0](); torch.cuda.synchronize()
