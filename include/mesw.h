@@ -189,6 +189,30 @@ typedef struct {
   int32_t x_corr_ld;
 } mesw_linear_args;
 
+/* ------------------------------------------- K3: prefill fused multi-expert linear
+ * Large token batches (prefill, BASELINE config 4): tokens come in 128-token groups, group g
+ * covering rows [128g, 128g+128) of the canonical x (NP rows, NP % 256 == 0) and using expert
+ * slot group_slot[g] (DEVICE int32 array, -1 = base only).  y[t, :] = x[t, :] . bf16(W +
+ * Dtilde_e) (+ residual): the delta is folded into the tensor-core A operand per unit
+ * (RN_bf16(W + s_j q_ij), salient inputs RN_bf16(W + half(R))), so the tensor work equals
+ * the dense base GEMM (Eq. 4; toylm.py:183-186 applies x.W + x.Dtilde).
+ * 2-bit codes (code_bits 2).  Same expert table / weight layouts as mesw_me_linear. */
+typedef struct {
+  const uint16_t* x;     /* canonical layout of NP rows                               */
+  int32_t NP, B, m, n;   /* NP: multiple of 256; rows >= B are not written            */
+  const uint16_t* w;
+  const mesw_expert_dev* expert_table;
+  int32_t code_bits;
+  const int32_t* group_slot; /* DEVICE [NP/128]                                       */
+  void* y;
+  int32_t y_bf16, ldy;
+  const uint16_t* residual;
+  int32_t ld_res;
+  int32_t num_ctas;      /* 0 = all SMs (CTA pairs)                                   */
+} mesw_prefill_args;
+
+int mesw_me_linear_prefill(const mesw_prefill_args* a, void* stream);
+
 /* Canonical activation layout consumed by mesw_me_linear: rows padded to
  * NP = ceil16(B); for each 128-wide k-step ks a tile of NP*128 bf16 split in two
  * halves h (rows 0-7 / 8-15 of every 16-row window -- the N split of a cta_group::2

@@ -40,9 +40,17 @@ class LinearArgs(C.Structure):
                 ("x_corr", C.c_void_p), ("x_corr_ld", C.c_int32)]
 
 
+class PrefillArgs(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("NP", C.c_int32), ("B", C.c_int32), ("m", C.c_int32), ("n", C.c_int32),
+                ("w", C.c_void_p), ("expert_table", C.c_void_p), ("code_bits", C.c_int32),
+                ("group_slot", C.c_void_p), ("y", C.c_void_p), ("y_bf16", C.c_int32), ("ldy", C.c_int32),
+                ("residual", C.c_void_p), ("ld_res", C.c_int32), ("num_ctas", C.c_int32)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/mesw.h
 _SIGNATURES = [
     ("mesw_abi_version", C.c_int, []),
+    ("mesw_me_linear_prefill", C.c_int, [C.POINTER(PrefillArgs), C.c_void_p]),
     ("mesw_last_error", C.c_char_p, []),
     ("mesw_device_sm_count", C.c_int, []),
     ("mesw_set_pdl", C.c_int, [C.c_int]),

@@ -433,6 +433,120 @@ class LinearPlan:
         _lib.check(self._fn(C.byref(self.args), _stream(stream)))
 
 
+PREFILL_GROUP = 128  # tokens per expert group of the prefill kernel (K3)
+PREFILL_TILE = 256
+
+
+class PrefillPlan:
+    """Pre-built launch of the prefill fused multi-expert linear (K3, mesw_me_linear_prefill).
+
+    `xc`: canonical layout of NP rows (NP % 256 == 0); `group_slots[g]` = expert-table slot of
+    rows [128g, 128g+128) or -1 (base only).  y[t] = x[t] . bf16(W + Dtilde_e): the delta is
+    folded into the tensor-core A operand, so the tensor work is the base GEMM's."""
+
+    def __init__(self, xc: torch.Tensor, NP: int, B: int, weight: DeviceWeight, table: ExpertTable | None,
+                 group_slots, out: torch.Tensor, residual: torch.Tensor | None = None, num_ctas: int = 0):
+        if NP % PREFILL_TILE or B > NP or B < 1:
+            raise ValueError("prefill: NP must be a multiple of 256 and 1 <= B <= NP")
+        geom = weight.geom
+        if xc.numel() < canonical_numel(NP, geom.m) or xc.dtype != torch.bfloat16:
+            raise ValueError("xc too small for the canonical layout of NP rows")
+        slots = [int(s) for s in group_slots]
+        if len(slots) != NP // PREFILL_GROUP:
+            raise ValueError("one slot per 128-token group")
+        if any(s >= 0 for s in slots) and (table is None or table.code_bits != 2):
+            raise NotImplementedError("prefill kernel: 2-bit codes only")
+        if out.stride(1) != 1 or out.dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("out must be a row-contiguous bf16/f32 tensor")
+        self.geom = geom
+        self.slots_dev = torch.as_tensor(slots, dtype=torch.int32, device=xc.device)
+        self.keep = (xc, weight, table, out, residual)
+        a = _lib.PrefillArgs()
+        a.x, a.NP, a.B, a.m, a.n = xc.data_ptr(), NP, B, geom.m, geom.n
+        a.w = weight.frag.data_ptr()
+        a.expert_table = table.dev.data_ptr() if table is not None else None
+        a.code_bits = 2
+        a.group_slot = self.slots_dev.data_ptr()
+        a.y, a.y_bf16, a.ldy = out.data_ptr(), 1 if out.dtype == torch.bfloat16 else 0, out.stride(0)
+        if residual is not None:
+            if residual.dtype != torch.bfloat16:
+                raise ValueError("residual must be bf16")
+            a.residual, a.ld_res = residual.data_ptr(), residual.stride(0)
+        a.num_ctas = num_ctas
+        self.args = a
+        self._fn = _lib.lib().mesw_me_linear_prefill
+
+    def __call__(self, stream=None) -> None:
+        _lib.check(self._fn(C.byref(self.args), _stream(stream)))
+
+
+def prefill_layout(B: int, segments) -> tuple:
+    """Rows -> prefill layout: every expert segment starts on a 128-row group boundary,
+    rows in no segment (base only) fill groups of their own.  Returns (NP, group_slots, src)
+    with src[new_row] = old row or -1 (padding)."""
+    segs = sorted((int(b), int(e), int(s)) for b, e, s in segments)
+    src, slots = [], []
+
+    def pad_to_group(slot):
+        while len(src) % PREFILL_GROUP:
+            src.append(-1)
+        return slot
+
+    cur = 0
+    for b, e, sl in segs:
+        if cur < b:  # base-only rows
+            start = len(src)
+            src.extend(range(cur, b))
+            pad_to_group(None)
+            slots.extend([-1] * ((len(src) - start) // PREFILL_GROUP))
+        start = len(src)
+        src.extend(range(b, e))
+        pad_to_group(None)
+        slots.extend([sl] * ((len(src) - start) // PREFILL_GROUP))
+        cur = e
+    if cur < B:
+        start = len(src)
+        src.extend(range(cur, B))
+        pad_to_group(None)
+        slots.extend([-1] * ((len(src) - start) // PREFILL_GROUP))
+    while len(src) % PREFILL_TILE:
+        src.extend([-1] * PREFILL_GROUP)
+        slots.append(-1)
+    return len(src), slots, src
+
+
+def me_linear_prefill(x: torch.Tensor, weight: DeviceWeight, table: ExpertTable | None, segments,
+                      out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
+                      out_dtype=torch.bfloat16, num_ctas: int = 0, stream=None) -> torch.Tensor:
+    """Prefill form of me_linear for large token batches (BASELINE config 4): rows grouped by
+    expert are laid out in 128-row groups (one device gather when segments are not already
+    128-aligned), one K3 launch, results returned in the caller's row order."""
+    geom = weight.geom
+    B = x.shape[0]
+    if out is None:
+        out = torch.empty((B, geom.n), dtype=out_dtype, device=x.device)
+    NP, slots, src = prefill_layout(B, segments)
+    xm = x[:, :geom.m] if x.shape[1] >= geom.m else x
+    aligned = src[:B] == list(range(B)) and all(v < 0 for v in src[B:])
+    if aligned:
+        xp = torch.zeros((NP, geom.m), dtype=torch.bfloat16, device=x.device)
+        xp[:B] = xm
+        PrefillPlan(pack_x(xp, stream=stream), NP, B, weight, table, slots, out, residual, num_ctas)(stream)
+        return out
+    src_t = torch.as_tensor(src, dtype=torch.int64, device=x.device)
+    valid = src_t >= 0
+    xp = torch.zeros((NP, geom.m), dtype=torch.bfloat16, device=x.device)
+    xp[valid] = xm[src_t[valid]]
+    rp = None
+    if residual is not None:
+        rp = torch.zeros((NP, residual.shape[1]), dtype=residual.dtype, device=x.device)
+        rp[valid] = residual[src_t[valid]]
+    yp = torch.empty((NP, out.shape[1]), dtype=out.dtype, device=x.device)
+    PrefillPlan(pack_x(xp, stream=stream), NP, NP, weight, table, slots, yp, rp, num_ctas)(stream)
+    out[src_t[valid]] = yp[valid]
+    return out
+
+
 # ------------------------------------------------------------------ launch-width tuning
 # K2 splits (column-group pair, k-step) units over CTA pairs (stream-K).  When the units
 # divide evenly into whole column groups or aligned k-splits, the final reduction has
