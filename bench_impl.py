@@ -103,15 +103,16 @@ def reference_arm(args):
     if args.config == "c4":
         for _ in range(min(args.warmup, 1)):
             _c4_cpu()
-        dts = [_c4_cpu() for _ in range(args.steps)]
+        dts = [_c4_cpu() * _C4_SCALE for _ in range(args.steps)]
         val = C4_T / (sum(dts) / len(dts))
-        return {"impl": "reference", "metric": "prefill tokens/sec, one Mistral MLP linear 4096x14336, 2048 tokens over 16 experts",
+        return {"impl": "reference", "metric": "prefill tokens/sec through a Mistral decoder layer's 4 fused linears, 2048 tokens over 16 experts",
                 "value": val, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * C4_T / val, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
-                "config": {"workload": "c4: prefill 2048 tokens x 16 experts (128 each), 4096x14336 fused linear"},
+                "config": {"workload": "c4: prefill 2048 tokens x 16 experts (128 each) through q|k|v, o, gate|up, down"},
                 "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
-                                 "sample": "per step: 1 expert group of 128 tokens (x_g@W + x_g@reconstruct), x16"},
+                                 "sample": "per step: 1 expert group of 128 tokens (x_g@W + x_g@reconstruct) of a "
+                                           "4096x14336 linear, x16 groups, scaled by the 4 linears' flops"},
                 "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     from bench_mistral import reference_arm_c2
     return reference_arm_c2(args)
@@ -315,83 +316,133 @@ def _c4_cpu(max_groups: int = 1):
     return (time.perf_counter() - t0) / max_groups * C4_E
 
 
+C4_KINDS = (("qkv", 4096, (4096, 1024, 1024)), ("o", 4096, (4096,)), ("gate_up", 4096, (14336, 14336)),
+            ("down", 14336, (4096,)))
+
+
 def run_c4(args, ws, rank, local, ClockSampler, peaks):
-    """C4: prefill of 2048 tokens (16 experts x 128) through one 4096x14336 fused linear:
-    base GEMM and delta contraction on tcgen05 (one launch per expert group of 128 rows)."""
+    """C4: prefill of 2048 tokens over 16 experts (128 tokens each) through the 4 fused linears
+    of a Mistral decoder layer (q|k|v, o, gate|up, down) with the K3 prefill kernel: the delta
+    is folded into the tcgen05 A operand, so the tensor work is the base GEMM's.  One step =
+    the 4 launches; 2 rotating weight/expert replicas (L2-cold weights)."""
     import json
     import torch
     from paper_2406_09041_b200 import compress, synth
-    from paper_2406_09041_b200.device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan,
+    from paper_2406_09041_b200.device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, PrefillPlan,
                                                pack_x)
-    geom = LinearGeometry(C1_M, (C1_N,))
     g = torch.Generator(device="cuda").manual_seed(rank)
-    dw = DeviceWeight.empty(geom)
-    dw.load_block(0, (torch.randn((C1_M, C1_N), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
-    table = ExpertTable("cuda")
-    for e in range(C4_E):
-        blob = synth.synthetic_expert_artifact(100 + e, [(C1_M, C1_N)], f"e{e}")
-        table.set(e, DeviceDelta.from_blocks([compress.deserialize_artifact(blob).layers[0]], geom))
-    per = C4_T // C4_E
-    x = torch.randn((C4_T, C1_M), generator=g, device="cuda").to(torch.bfloat16)
-    y = torch.empty((C4_T, C1_N), dtype=torch.bfloat16, device="cuda")
-    plans = [LinearPlan(pack_x(x[e * per:(e + 1) * per].contiguous()), per, dw, table, [(0, per, e)],
-                        y[e * per:(e + 1) * per], geom=geom) for e in range(C4_E)]
-    for _ in range(args.warmup):
-        for p in plans:
-            p()
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    stream = torch.cuda.current_stream()
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        st.record(stream)
-        for _ in range(args.steps):
-            for p in plans:
-                p()
-        en.record(stream)
+    groups = C4_T // 128
+    slots = [gi * C4_E // groups for gi in range(groups)]
+    reps = 2
+    kinds = []
+    for name, m, blocks in C4_KINDS:
+        geom = LinearGeometry(m, blocks)
+        x = torch.randn((C4_T, m), generator=g, device="cuda").to(torch.bfloat16)
+        xc = pack_x(x)
+        y = torch.empty((C4_T, geom.n), dtype=torch.bfloat16, device="cuda")
+        fused, base = [], []
+        for r in range(reps):
+            dw = DeviceWeight.empty(geom)
+            for bi, nb in enumerate(blocks):
+                dw.load_block(bi, (torch.randn((m, nb), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+            table = ExpertTable("cuda")
+            for e in range(C4_E):
+                blob = synth.synthetic_expert_artifact(100 * r + e, [(m, nb) for nb in blocks], f"e{e}")
+                table.set(e, DeviceDelta.from_blocks(compress.deserialize_artifact(blob).layers, geom))
+                del blob
+            fused.append(PrefillPlan(xc, C4_T, C4_T, dw, table, slots, y))
+            base.append(PrefillPlan(xc, C4_T, C4_T, dw, None, [-1] * groups, y))
+        kinds.append((name, m, sum(blocks), fused, base, x))
+
+    def run_all(which, i):
+        for k in kinds:
+            k[3 if which == "fused" else 4][i % reps]()
+
+    def timed(which, steps, clk=None):
+        for i in range(args.warmup):
+            run_all(which, i)
         torch.cuda.synchronize()
-    ms_t = torch.tensor([st.elapsed_time(en) / args.steps], device="cuda")
+        if ws > 1:
+            torch.distributed.barrier()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for i in range(steps):
+            run_all(which, i)
+        en.record()
+        torch.cuda.synchronize()
+        return st.elapsed_time(en) / steps
+
+    with ClockSampler(local) as clk:
+        ms = timed("fused", args.steps)
+    ms_base = timed("base", args.steps)
+    per_kind = {}
+    for name, m, n, fused, base, _ in kinds:  # per-kind time of the fused launch
+        for i in range(3):
+            fused[i % reps]()
+        torch.cuda.synchronize()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for i in range(args.steps):
+            fused[i % reps]()
+        en.record()
+        torch.cuda.synchronize()
+        t = st.elapsed_time(en) / args.steps
+        per_kind[name] = {"ms": t, "tflops": 2.0 * C4_T * m * n / (t / 1e3) / 1e12}
+    ms_t = torch.tensor([ms], device="cuda")
     if ws > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     ms = float(ms_t.item())
-    flops = 2.0 * C4_T * C1_M * C1_N * 2  # base + delta contraction
+    flops = sum(2.0 * C4_T * m * n for _, m, n, _, _, _ in kinds)  # base GEMM flops of the 4 linears
     with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
         pk = json.load(f)
     peak = float(pk.get("bf16_tflops", 1590.0))
     achieved = flops / (ms / 1e3) / 1e12
-    # e2e: host x (pinned) -> device, pack + fused launches, y -> host
-    xh = x.cpu().pin_memory()
-    yh = torch.empty((C4_T, C1_N), dtype=torch.bfloat16).pin_memory()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        x.copy_(xh, non_blocking=True)
-        for e, p in enumerate(plans):
-            pack_x(x[e * per:(e + 1) * per].contiguous(), out=p.keep[0])  # canonical layout of the fresh input
+    for v in per_kind.values():
+        v["frac"] = v["tflops"] / peak
+    # e2e through the public API: host x (pinned) -> device -> canonical layout -> 4 launches -> y -> host
+    xh = [k[5].cpu().pin_memory() for k in kinds]
+    yh = [torch.empty((C4_T, k[2]), dtype=torch.bfloat16).pin_memory() for k in kinds]
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+        for (name, m, n, fused, base, x), h, yo in zip(kinds, xh, yh):
+            x.copy_(h, non_blocking=True)
+            p = fused[i % reps]
+            pack_x(x, out=p.keep[0])
             p()
-        yh.copy_(y, non_blocking=True)
+            yo.copy_(p.keep[3][:, :n], non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e2e_s = (time.perf_counter() - t0) / args.steps
     line = {
-        "metric": "prefill tokens/sec, one Mistral MLP linear 4096x14336, 2048 tokens over 16 experts",
+        "metric": "prefill tokens/sec through a Mistral decoder layer's 4 fused linears, 2048 tokens over 16 experts",
         "value": ws * C4_T / (ms / 1e3), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "c4: prefill 2048 tokens x 16 experts (128 each), 4096x14336 fused linear",
-                   "launches_per_step": C4_E},
+        "config": {"workload": "c4: prefill 2048 tokens x 16 experts (128 each) through q|k|v, o, gate|up, down "
+                               "(one decoder layer's fused linears, K3 kernel)", "launches_per_step": len(kinds),
+                   "l2": "2 rotating weight/expert replicas per linear (> 126 MB L2)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": "measured burst",
-                     "flops_per_step": flops, "kernel": "me_linear_tc_kernel<2>"},
-        "e2e": {"value": ws * C4_T / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(xh.numel() * 2),
-                "d2h_bytes_per_step": int(yh.numel() * 2)},
-        "gpu_launches": C4_E * args.steps,
+                     "frac": achieved / peak, "traffic": None, "peak_kind": "measured burst (bf16_tflops)",
+                     "flops_per_step": flops, "flops_note": "base GEMM flops; the delta is folded into the A "
+                                                           "operand and adds no tensor flops",
+                     "base_only_ms": ms_base, "base_only_frac": flops / (ms_base / 1e3) / 1e12 / peak,
+                     "per_kind": per_kind, "kernel": "me_linear_prefill_kernel (K3)"},
+        "e2e": {"value": ws * C4_T / e2e_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(sum(h.numel() * 2 for h in xh)),
+                "d2h_bytes_per_step": int(sum(v.numel() * 2 for v in yh))},
+        "gpu_launches": len(kinds) * args.steps,
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:
-        dt = _c4_cpu()
+        dt = _c4_cpu() * _C4_SCALE
         line["cpu_baseline"] = {"value": C4_T / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-                                "sample": "1 expert group of 128 tokens (x_g@W + x_g@reconstruct) timed, x16"}
+                                "sample": "1 expert group of 128 tokens (x_g@W + x_g@reconstruct) of a 4096x14336 "
+                                          "linear timed, x16 groups, scaled by the 4 linears' flops"}
     return line
+
+
+_C4_SCALE = sum(m * sum(b) for _, m, b in C4_KINDS) / (C1_M * C1_N)  # 4 layer linears vs one 4096x14336
 
 
 def run_ours(args, ws, rank, local, ClockSampler, peaks):

@@ -19,8 +19,8 @@
 // Work: tiles (column-group pair, 256-token tile = two 128-token expert groups), persistent
 // CTA pairs walk tiles cg-pair-major so the pairs running at the same time share W tiles in L2.
 // Roles per CTA (16 warps):
-//   warp 0      producer: W unit (32 KiB), this CTA's half of the x tile (32 KiB: 2 groups x 8
-//               windows x 2 KiB), the two groups' code units (4 KiB each) -> smem rings.
+//   warps 0, 2  producers (one thread each): W unit (32 KiB) + the two groups' code units
+//               (4 KiB each); this CTA's half of the x tile (32 KiB: 2 groups x 8 windows x 2 KiB).
 //   warp 1      leader: MMA issuer (M = 256 over the pair, N = 128 per group, K = 16);
 //               peer: relays "x half landed" to the leader's barrier.
 //   warps 4-11  two merge groups: group g owns k-half g of every unit, thread = output row;
@@ -45,7 +45,7 @@ constexpr int kGroupTok = 128;
 constexpr int kASlots = 4;
 constexpr int kACols = 64;
 constexpr int kAccCols = 2 * kGroupTok;
-constexpr int kNW = 3, kNX = 3, kNC = 4;  // ring depths (W / x / codes)
+constexpr int kNW = 2, kNX = 4, kNC = 4;  // ring depths (W / x / codes): x is held until the MMAs finish
 constexpr int kXBytes = kTileTok / 2 * kUnitK * 2;  // this CTA's half of the x tile: 32 KiB
 constexpr int kCBytes = 2 * 4096;                   // two groups' 2-bit code units
 constexpr int kSmemBytes = 232448;
@@ -123,15 +123,19 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
   const uint32_t tbase = S.tmem_base;
   pdl_trigger();
 
-  if (warp == 0) {
-    // ============================ producer ============================
+  if (warp == 0 || warp == 2) {
+    // ============================ producers ============================
+    // warp 0: W units + code units (consumed by the merge warps, freed right after their LDS);
+    // warp 2: x half-tiles (held until the k-step's MMAs complete).  Separate threads, so a
+    // full x ring never holds back the weight stream.
     if (lane == 0) {
       uint64_t evict_first;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
-      int sw = 0, sx = 0, sc = 0;
-      uint32_t pw = 0, px = 0, pcp = 0;
-      bool fw = true, fx = true, fc = true;
-      pdl_wait();
+      int s_ = 0;
+      uint32_t ph = 0, pc2 = 0;
+      int sc = 0;
+      bool first = true, cfirst = true;
+      if (warp == 2) pdl_wait();  // x is the previous kernel's output; W / codes are static
       for (int tile = c2; tile < p.n_tiles; tile += G2) {
         const int cgp = tile / p.n_tt, tt = tile % p.n_tt;
         const int cg = 2 * cgp + (int)rank;
@@ -140,22 +144,27 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
         const uint8_t* c1 = s1 >= 0 ? reinterpret_cast<const uint8_t*>(p.table[s1].codes) : nullptr;
         for (int ks = 0; ks < p.n_ks; ++ks) {
           const size_t unit = (size_t)cg * p.n_ks + ks;
-          if (!fw) mbar_wait(&S.wempty[sw], pw ^ 1);
-          mbar_arrive_expect_tx(&S.wfull[sw], kUnitWBytes);
-          bulk_g2s(ring + kWOff + (size_t)sw * kUnitWBytes, p.w + unit * kUnitWBytes, kUnitWBytes, &S.wfull[sw]);
-          if (++sw == kNW) { sw = 0; pw ^= 1; fw = false; }
-          if (!fc) mbar_wait(&S.cempty[sc], pcp ^ 1);
-          mbar_arrive_expect_tx(&S.cfull[sc], (c0 ? 4096u : 0u) + (c1 ? 4096u : 0u));
-          uint8_t* cdst = ring + kCOff + (size_t)sc * kCBytes;
-          if (c0) bulk_g2s_hint(cdst, c0 + unit * 4096, 4096, &S.cfull[sc], evict_first);
-          if (c1) bulk_g2s_hint(cdst + 4096, c1 + unit * 4096, 4096, &S.cfull[sc], evict_first);
-          if (++sc == kNC) { sc = 0; pcp ^= 1; fc = false; }
-          if (!fx) mbar_wait(&S.xempty[sx], px ^ 1);
-          mbar_arrive_expect_tx(&S.xfull[sx], kXBytes);
-          // this CTA's half of 16 windows starting at window 16*tt of k-step ks
-          const size_t xoff = (size_t)ks * p.NP * kUnitK + (size_t)rank * (p.NP / 2) * kUnitK + (size_t)tt * 16 * 1024;
-          bulk_g2s(ring + kXOff + (size_t)sx * kXBytes, p.x + xoff, kXBytes, &S.xfull[sx]);
-          if (++sx == kNX) { sx = 0; px ^= 1; fx = false; }
+          if (warp == 0) {
+            if (!first) mbar_wait(&S.wempty[s_], ph ^ 1);
+            mbar_arrive_expect_tx(&S.wfull[s_], kUnitWBytes);
+            bulk_g2s_hint(ring + kWOff + (size_t)s_ * kUnitWBytes, p.w + unit * kUnitWBytes, kUnitWBytes,
+                          &S.wfull[s_], evict_first);
+            if (++s_ == kNW) { s_ = 0; ph ^= 1; first = false; }
+            if (!cfirst) mbar_wait(&S.cempty[sc], pc2 ^ 1);
+            mbar_arrive_expect_tx(&S.cfull[sc], (c0 ? 4096u : 0u) + (c1 ? 4096u : 0u));
+            uint8_t* cdst = ring + kCOff + (size_t)sc * kCBytes;
+            if (c0) bulk_g2s_hint(cdst, c0 + unit * 4096, 4096, &S.cfull[sc], evict_first);
+            if (c1) bulk_g2s_hint(cdst + 4096, c1 + unit * 4096, 4096, &S.cfull[sc], evict_first);
+            if (++sc == kNC) { sc = 0; pc2 ^= 1; cfirst = false; }
+          } else {
+            if (!first) mbar_wait(&S.xempty[s_], ph ^ 1);
+            mbar_arrive_expect_tx(&S.xfull[s_], kXBytes);
+            // this CTA's half of 16 windows starting at window 16*tt of k-step ks
+            const size_t xoff =
+                (size_t)ks * p.NP * kUnitK + (size_t)rank * (p.NP / 2) * kUnitK + (size_t)tt * 16 * 1024;
+            bulk_g2s(ring + kXOff + (size_t)s_ * kXBytes, p.x + xoff, kXBytes, &S.xfull[s_]);
+            if (++s_ == kNX) { s_ = 0; ph ^= 1; first = false; }
+          }
         }
       }
     }
@@ -222,12 +231,13 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
       uint32_t s2[2];
       const int32_t* sal_idx[2];
       const uint16_t* sal_rows[2];
-      int sal_r[2], sal_end[2];
+      int sal_r[2], sal_end[2], sal_next[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         slot_e[e] = p.group_slot[2 * tt + e];
         s2[e] = 0;
         sal_r[e] = sal_end[e] = 0;
+        sal_next[e] = 1 << 30;
         sal_idx[e] = nullptr;
         sal_rows[e] = nullptr;
         if (slot_e[e] >= 0) {
@@ -237,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
           sal_end[e] = ex.sal_off[cg + 1];
           sal_idx[e] = ex.sal_idx;
           sal_rows[e] = ex.sal_rows;
+          if (sal_r[e] < sal_end[e]) sal_next[e] = sal_idx[e][sal_r[e]];  // one global read per hit, not per k-step
         }
       }
       for (int ks = 0; ks < p.n_ks; ++ks) {
@@ -280,18 +291,20 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
           // salient inputs of this k-half (their codes are q = 0): rewrite the pair word with
           // RN_bf16(W + half(R)) by a single-column store after the tile store (rare: k = 8 rows
           // per block)
-          while (slot_e[e] >= 0 && sal_r[e] < sal_end[e] && sal_idx[e][sal_r[e]] < k0 + 64) {
-            const int i = sal_idx[e][sal_r[e]] - k0;
+          while (sal_next[e] < k0 + 64) {
+            const int i = sal_next[e] - k0;
             const float r0v = __half2float(__ushort_as_half(sal_rows[e][(size_t)sal_r[e] * kUnitN + mrow]));
             ++sal_r[e];
+            sal_next[e] = sal_r[e] < sal_end[e] ? sal_idx[e][sal_r[e]] : (1 << 30);
             if (i < 0) continue;  // belongs to the other group's k-half
             const int pw = i >> 1;
             bool lo_s = (i & 1) == 0, hi_s = !lo_s;
             float r_lo = lo_s ? r0v : 0.f, r_hi = lo_s ? 0.f : r0v;
-            if (lo_s && sal_r[e] < sal_end[e] && sal_idx[e][sal_r[e]] == k0 + i + 1) {  // both halves salient
+            if (lo_s && sal_next[e] == k0 + i + 1) {  // both halves of the pair salient
               hi_s = true;
               r_hi = __half2float(__ushort_as_half(sal_rows[e][(size_t)sal_r[e] * kUnitN + mrow]));
               ++sal_r[e];
+              sal_next[e] = sal_r[e] < sal_end[e] ? sal_idx[e][sal_r[e]] : (1 << 30);
             }
             uint32_t ww = 0, cword = 0;
 #pragma unroll
