@@ -38,8 +38,14 @@
 namespace mesw {
 namespace prefill {
 
-constexpr int kThreads = 512;
-constexpr int kMergeWarp0 = 4, kEpiWarp0 = 12;
+#ifndef MESW_PF_GROUPS
+#define MESW_PF_GROUPS 4
+#endif
+constexpr int kMergeGroups = MESW_PF_GROUPS;        // merge groups: group g owns k-slice g of every unit
+constexpr int kSliceK = kUnitK / kMergeGroups;      // inputs per slice (32 at 4 groups)
+constexpr int kSliceW = kSliceK / 2;                // bf16x2 words per slice (16)
+constexpr int kMergeWarp0 = 4, kEpiWarp0 = kMergeWarp0 + 4 * kMergeGroups;
+constexpr int kThreads = (kEpiWarp0 + 4) * 32;
 constexpr int kTileTok = 256;      // tokens per tile (two 128-token groups)
 constexpr int kGroupTok = 128;
 constexpr int kASlots = 4;
@@ -86,13 +92,35 @@ __device__ __forceinline__ uint32_t bf16x2_of(float v) {
   return d;
 }
 
-// merged A words for one k-half: a[i] = RN_bf16x2(q_pair * s + w_pair) (single rounding)
-__device__ __forceinline__ void merge_half(const uint32_t* wv, const uint32_t* cw, uint32_t s2, uint32_t* a) {
-  uint32_t q[32];
-  dequant_chunk<2>(cw, q);  // exact bf16 q in {-2,-1,0,1}
+// merged A words of one k-slice: a[i] = RN_bf16x2(q_pair * s + w_pair) (single rounding).  cw:
+// the slice's code words (8 pairs each: lo code at bit 2l, hi at 16 + 2l -- mesw_layout.cuh)
+__device__ __forceinline__ void merge_slice(const uint32_t* wv, const uint32_t* cw, uint32_t s2, uint32_t* a) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) a[i] = bf16x2_fma(q[i], s2, wv[i]);
+  for (int w = 0; w < kSliceW / 8; ++w) {
+    const uint32_t c = cw[w], b = c >> 6, d = c >> 12;
+    uint32_t q[8];  // exact bf16 q in {-2,-1,0,1} (dequant_chunk<2> magic-number form)
+    q[0] = bf16x2_fma(lop3_and_or(c, 0x00030003u, 0x43004300u), 0x3F803F80u, 0xC302C302u);
+    q[1] = bf16x2_fma(lop3_and_or(c, 0x000C000Cu, 0x43004300u), 0x3E803E80u, 0xC208C208u);
+    q[2] = bf16x2_fma(lop3_and_or(c, 0x00300030u, 0x43004300u), 0x3D803D80u, 0xC120C120u);
+    q[3] = bf16x2_fma(lop3_and_or(b, 0x00030003u, 0x43004300u), 0x3F803F80u, 0xC302C302u);
+    q[4] = bf16x2_fma(lop3_and_or(b, 0x000C000Cu, 0x43004300u), 0x3E803E80u, 0xC208C208u);
+    q[5] = bf16x2_fma(lop3_and_or(b, 0x00300030u, 0x43004300u), 0x3D803D80u, 0xC120C120u);
+    q[6] = bf16x2_fma(lop3_and_or(d, 0x00030003u, 0x43004300u), 0x3F803F80u, 0xC302C302u);
+    q[7] = bf16x2_fma(lop3_and_or(d, 0x000C000Cu, 0x43004300u), 0x3E803E80u, 0xC208C208u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[8 * w + i] = bf16x2_fma(q[i], s2, wv[8 * w + i]);
+  }
 }
+
+#define MESW_R8(b) "r"(r[b + 0]), "r"(r[b + 1]), "r"(r[b + 2]), "r"(r[b + 3]), "r"(r[b + 4]), "r"(r[b + 5]), "r"(r[b + 6]), "r"(r[b + 7])
+__device__ __forceinline__ void tmem_st_slice(uint32_t taddr, const uint32_t* r) {
+  if constexpr (kSliceW == 16)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(taddr), MESW_R8(0), MESW_R8(8) : "memory");
+  else
+    tmem_st32(taddr, r);
+}
+#undef MESW_R8
 
 __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -103,10 +131,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
   const int c2 = blockIdx.x >> 1, G2 = p.G >> 1;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kNW; ++i) { mbar_init(&S.wfull[i], 1); mbar_init(&S.wempty[i], 8); }
+    for (int i = 0; i < kNW; ++i) { mbar_init(&S.wfull[i], 1); mbar_init(&S.wempty[i], 4 * kMergeGroups); }
     for (int i = 0; i < kNX; ++i) { mbar_init(&S.xfull[i], rank == 0 ? 2 : 1); mbar_init(&S.xempty[i], 1); }
-    for (int i = 0; i < kNC; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 8); }
-    for (int i = 0; i < kASlots; ++i) { mbar_init(&S.afull[i], 16); mbar_init(&S.aempty[i], 1); }
+    for (int i = 0; i < kNC; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 4 * kMergeGroups); }
+    for (int i = 0; i < kASlots; ++i) { mbar_init(&S.afull[i], 2 * 4 * kMergeGroups); mbar_init(&S.aempty[i], 1); }
     mbar_init(&S.accfull, 1);
     mbar_init(&S.accempty, 8);
     fence_mbar_init();
@@ -217,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
     }
   } else if (warp >= kMergeWarp0 && warp < kEpiWarp0) {
     // ============================ merge groups ============================
-    const int g = (warp - kMergeWarp0) >> 2;  // k-half of every unit
+    const int g = (warp - kMergeWarp0) >> 2;  // k-slice of every unit
     const int quarter = warp & 3, mrow = quarter * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     int sw = 0, sc = 0;
@@ -252,51 +280,55 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
       }
       for (int ks = 0; ks < p.n_ks; ++ks) {
         mbar_wait(&S.wfull[sw], pw);
-        uint32_t wv[32];
+        uint32_t wv[kSliceW];
         const uint8_t* wt = ring + kWOff + (size_t)sw * kUnitWBytes;
+        constexpr int kChunks = kSliceK / 8;  // 16-byte k-chunks of the slice
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // k-chunks 8g..8g+7 of row mrow
-          const uint4 t4 = lds128(wt + (mrow >> 3) * 2048 + (8 * g + c) * 128 + (mrow & 7) * 16);
+        for (int c = 0; c < kChunks; ++c) {
+          const uint4 t4 = lds128(wt + (mrow >> 3) * 2048 + (kChunks * g + c) * 128 + (mrow & 7) * 16);
           wv[4 * c] = t4.x; wv[4 * c + 1] = t4.y; wv[4 * c + 2] = t4.z; wv[4 * c + 3] = t4.w;
         }
         mbar_wait(&S.cfull[sc], pcp);
-        uint32_t cw[2][4];
+        constexpr int kCW = kSliceW / 8;  // code words of the slice
+        uint32_t cw[2][kCW];
         const uint8_t* ct = ring + kCOff + (size_t)sc * kCBytes;
+        // slice g: k-half kh = (g * kSliceK) / 64, words from ((g * kSliceK) % 64) / 16
+        const int kh = (g * kSliceK) >> 6, w0 = ((g * kSliceK) & 63) >> 4;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint4 t4 = lds128(ct + (size_t)e * 4096 + ((size_t)g * 128 + mrow) * 16);
-          cw[e][0] = t4.x; cw[e][1] = t4.y; cw[e][2] = t4.z; cw[e][3] = t4.w;
-        }
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int w = 0; w < kCW; ++w)
+            cw[e][w] = *reinterpret_cast<const uint32_t*>(ct + (size_t)e * 4096 + ((size_t)kh * 128 + mrow) * 16 + (w0 + w) * 4);
         __syncwarp();
         if (lane == 0) { mbar_arrive(&S.wempty[sw]); mbar_arrive(&S.cempty[sc]); }
         if (++sw == kNW) { sw = 0; pw ^= 1; }
         if (++sc == kNC) { sc = 0; pcp ^= 1; }
-        const int k0 = ks * kUnitK + g * 64;  // first input channel of this k-half
+        const int k0 = ks * kUnitK + g * kSliceK;  // first input channel of this k-slice
         int slots[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e, ++job) {
           const int slot = (int)(job % kASlots);
           slots[e] = slot;
           if (job >= kASlots) mbar_wait(&S.aempty[slot], ((job / kASlots) - 1) & 1);
-          const uint32_t acol = tbase + lane_addr + (uint32_t)(kAccCols + slot * kACols + g * 32);
+          const uint32_t acol = tbase + lane_addr + (uint32_t)(kAccCols + slot * kACols + g * kSliceW);
           {
-            uint32_t a[32];
-            if (slot_e[e] >= 0) merge_half(wv, cw[e], s2[e], a);
+            uint32_t a[kSliceW];
+            if (slot_e[e] >= 0) merge_slice(wv, cw[e], s2[e], a);
             else {
 #pragma unroll
-              for (int w = 0; w < 32; ++w) a[w] = wv[w];  // base-only group
+              for (int w = 0; w < kSliceW; ++w) a[w] = wv[w];  // base-only group
             }
-            tmem_st32(acol, a);
+            tmem_st_slice(acol, a);
           }
           // salient inputs of this k-half (their codes are q = 0): rewrite the pair word with
           // RN_bf16(W + half(R)) by a single-column store after the tile store (rare: k = 8 rows
           // per block)
-          while (sal_next[e] < k0 + 64) {
+          while (sal_next[e] < k0 + kSliceK) {
             const int i = sal_next[e] - k0;
             const float r0v = __half2float(__ushort_as_half(sal_rows[e][(size_t)sal_r[e] * kUnitN + mrow]));
             ++sal_r[e];
             sal_next[e] = sal_r[e] < sal_end[e] ? sal_idx[e][sal_r[e]] : (1 << 30);
-            if (i < 0) continue;  // belongs to the other group's k-half
+            if (i < 0) continue;  // belongs to another group's k-slice
             const int pw = i >> 1;
             bool lo_s = (i & 1) == 0, hi_s = !lo_s;
             float r_lo = lo_s ? r0v : 0.f, r_hi = lo_s ? 0.f : r0v;
@@ -308,9 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
             }
             uint32_t ww = 0, cword = 0;
 #pragma unroll
-            for (int w = 0; w < 32; ++w) ww = (w == pw) ? wv[w] : ww;
+            for (int w = 0; w < kSliceW; ++w) ww = (w == pw) ? wv[w] : ww;
 #pragma unroll
-            for (int w = 0; w < 4; ++w) cword = (w == (pw >> 3)) ? cw[e][w] : cword;
+            for (int w = 0; w < kCW; ++w) cword = (w == (pw >> 3)) ? cw[e][w] : cword;
             const int sh = 2 * (pw & 7);
             const float sf = bf16_lo(s2[e]);
             const float qlo = (float)((int)((cword >> sh) & 3u) - 2), qhi = (float)((int)((cword >> (16 + sh)) & 3u) - 2);
