@@ -28,6 +28,8 @@
 //   warps 12-15 epilogue: tcgen05.ld of the 2 x 128-column accumulators, y stores.
 // TMEM: accumulators [group 0 | group 1] x 128 columns, then 4 A slots of 64 columns.
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "mesw_common.cuh"
@@ -67,6 +69,7 @@ struct Params {
   const uint16_t* residual;
   int ld_res;
   int n_tiles, n_tt, G;  // tiles, 256-token tiles, CTAs
+  unsigned long long* prof;  // MESW_PF_PROF: leader issuer cycle counters per CTA pair (else null)
 };
 
 struct Smem {
@@ -74,7 +77,7 @@ struct Smem {
   uint64_t xfull[kNX], xempty[kNX];
   uint64_t cfull[kNC], cempty[kNC];
   uint64_t afull[kASlots], aempty[kASlots];
-  uint64_t accfull, accempty;
+  uint64_t accfull, accempty[2];
   uint32_t tmem_base;
 };
 
@@ -136,7 +139,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
     for (int i = 0; i < kNC; ++i) { mbar_init(&S.cfull[i], 1); mbar_init(&S.cempty[i], 4 * kMergeGroups); }
     for (int i = 0; i < kASlots; ++i) { mbar_init(&S.afull[i], 2 * 4 * kMergeGroups); mbar_init(&S.aempty[i], 1); }
     mbar_init(&S.accfull, 1);
-    mbar_init(&S.accempty, 8);
+    mbar_init(&S.accempty[0], 8);
+    mbar_init(&S.accempty[1], 8);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -217,31 +221,45 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
       uint32_t px = 0;
       uint32_t job = 0;  // A-slot sequence: 2 per k-step
       int n_t = 0;
+      long long pr[5] = {0, 0, 0, 0, 0};  // accempty, xfull, afull, issue, total (MESW_PF_PROF)
+      const long long t_start = clock64();
+      long long tq = 0;
       for (int tile = c2; tile < p.n_tiles; tile += G2, ++n_t) {
-        if (n_t > 0) {
-          mbar_wait_cluster(&S.accempty, (uint32_t)((n_t - 1) & 1));
-          tc_fence_after();
-        }
+
         for (int ks = 0; ks < p.n_ks; ++ks) {
+          if (p.prof) tq = clock64();
           mbar_wait_cluster(&S.xfull[sx], px);
+          if (p.prof) pr[1] += clock64() - tq;
           const uint64_t xd = xdesc0 + (uint64_t)(sx * (kXBytes >> 4));
 #pragma unroll 1
           for (int g = 0; g < 2; ++g, ++job) {
             const int slot = (int)(job % kASlots);
+            if (ks == 0 && n_t > 0) {  // group g's accumulator drained by the previous tile's epilogue
+              if (p.prof) tq = clock64();
+              mbar_wait_cluster(&S.accempty[g], (uint32_t)((n_t - 1) & 1));
+              tc_fence_after();
+              if (p.prof) pr[0] += clock64() - tq;
+            }
+            if (p.prof) tq = clock64();
             mbar_wait_cluster(&S.afull[slot], (job / kASlots) & 1);
             tc_fence_after();
+            if (p.prof) { pr[2] += clock64() - tq; tq = clock64(); }
             const uint32_t d = tbase + (uint32_t)(g * kGroupTok);
             const uint32_t a = tbase + (uint32_t)(kAccCols + slot * kACols);
             // group g's 8 windows: 8 x 2 KiB into this CTA's half tile
             const uint64_t bd = xd + (uint64_t)(g * 8 * (kXRowGroupBytes >> 4));
             mma2_ts_k128(uni(d), uni(a), uni64(bd), uni(id), uni(ks > 0 ? 1u : 0u));
             tc2_commit_w(&S.aempty[slot]);
+            if (p.prof) pr[3] += clock64() - tq;
           }
           tc2_commit_w(&S.xempty[sx]);
           if (++sx == kNX) { sx = 0; px ^= 1; }
         }
         tc2_commit_w(&S.accfull);
       }
+      pr[4] = clock64() - t_start;
+      if (p.prof && lane == 0)
+        for (int i = 0; i < 5; ++i) p.prof[(size_t)c2 * 8 + i] = (unsigned long long)pr[i];
     }
   } else if (warp >= kMergeWarp0 && warp < kEpiWarp0) {
     // ============================ merge groups ============================
@@ -376,33 +394,52 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
     for (int tile = c2; tile < p.n_tiles; tile += G2, ++n_t) {
       const int cgp = tile / p.n_tt, tt = tile % p.n_tt;
       const int j = (2 * cgp + (int)rank) * kUnitN + mrow;
+      const bool jok = j < p.n;
       mbar_wait_sleep(&S.accfull, (uint32_t)(n_t & 1));
       tc_fence_after();
+      // Group e's 128 columns: [h = 0: CTA0's B rows = window rows 0-7 | h = 1: rows 8-15], each
+      // 8 windows x 8 rows; 32 columns (4 windows) per tcgen05.ld.  Each group's accumulator is
+      // released as soon as it is drained, so the next tile's first MMAs of group 0 overlap
+      // the drain of group 1.
 #pragma unroll 1
-      for (int c0 = 0; c0 < kAccCols; c0 += 16) {
-        float v[16];
-        tmem_ld16(tbase + lane_addr + (uint32_t)c0, v);
-        if (j >= p.n) continue;
-        const int e = c0 / kGroupTok, cc = c0 % kGroupTok;
+      for (int e = 0; e < 2; ++e) {
+        const int t_e = tt * kTileTok + e * kGroupTok;  // first token of the group
+        const bool fast = jok && p.y_bf16 && !p.residual && t_e + kGroupTok <= p.B;
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {  // (h, window quad)
+          const int h = q >> 1, wq = q & 1;
+          uint32_t r[32];
+          tmem_ld32_nowait(tbase + lane_addr + (uint32_t)(e * kGroupTok + h * 64 + wq * 32), r);
+          tmem_ld_wait();
+          const int tq = t_e + 8 * h + wq * 4 * 16;  // token of column 0 of this load
+          if (fast) {
+            __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(p.y) + (size_t)tq * p.ldy + j;
+            const size_t ld = (size_t)p.ldy;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = cc + i;  // D column of group e: < 64 -> CTA0 rows (window rows 0-7), else rows 8-15
-          const int h = col >= 64 ? 1 : 0, r = col - 64 * h;
-          const int t = tt * kTileTok + e * kGroupTok + (r >> 3) * 16 + 8 * h + (r & 7);
-          if (t >= p.B) continue;
-          float y = v[i];
-          if (p.residual) y += bf16_to_f32(p.residual[(size_t)t * p.ld_res + j]);
-          if (p.y_bf16)
-            reinterpret_cast<__nv_bfloat16*>(p.y)[(size_t)t * p.ldy + j] = __float2bfloat16_rn(y);
-          else
-            reinterpret_cast<float*>(p.y)[(size_t)t * p.ldy + j] = y;
+            for (int w = 0; w < 4; ++w)
+#pragma unroll
+              for (int rr = 0; rr < 8; ++rr)
+                yp[(size_t)(w * 16 + rr) * ld] = __float2bfloat16_rn(__uint_as_float(r[w * 8 + rr]));
+          } else if (jok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int t = tq + (i >> 3) * 16 + (i & 7);
+              if (t >= p.B) continue;
+              float yv = __uint_as_float(r[i]);
+              if (p.residual) yv += bf16_to_f32(p.residual[(size_t)t * p.ld_res + j]);
+              if (p.y_bf16)
+                reinterpret_cast<__nv_bfloat16*>(p.y)[(size_t)t * p.ldy + j] = __float2bfloat16_rn(yv);
+              else
+                reinterpret_cast<float*>(p.y)[(size_t)t * p.ldy + j] = yv;
+            }
+          }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (rank == 0) mbar_arrive(&S.accempty);
-        else mbar_arrive_cta(&S.accempty, 0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&S.accempty[e]);
+          else mbar_arrive_cta(&S.accempty[e], 0);
+        }
       }
     }
   }
@@ -420,6 +457,16 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_prefill_kernel(const __
 }  // namespace mesw
 
 using namespace mesw;
+
+static unsigned long long* g_pf_prof = nullptr;
+
+// Debug (tools/pf_timing.py): copy the last MESW_PF_PROF launch's per-pair issuer counters
+// [pair][8] = {wait accempty, wait x, wait A slots, MMA issue + commit, total} in SM cycles.
+extern "C" int mesw_prefill_profile_copy(unsigned long long* h_out, int n) {
+  if (!g_pf_prof) return mesw_fail(MESW_ERR_VALUE, "no profile buffer (set MESW_PF_PROF)");
+  cudaError_t e = cudaMemcpy(h_out, g_pf_prof, (size_t)n * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? MESW_OK : mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
+}
 
 extern "C" int mesw_me_linear_prefill(const mesw_prefill_args* a, void* stream) {
   using namespace mesw::prefill;
@@ -446,6 +493,11 @@ extern "C" int mesw_me_linear_prefill(const mesw_prefill_args* a, void* stream) 
   p.n_tiles = (p.n_cg / 2) * p.n_tt;
   const int want = (a->num_ctas > 0 ? a->num_ctas : sms) / 2;
   p.G = 2 * std::max(1, std::min(want, p.n_tiles));
+  static const bool prof = getenv("MESW_PF_PROF") != nullptr;
+  if (prof) {
+    if (!g_pf_prof) cudaMalloc(&g_pf_prof, 1024 * 8 * sizeof(unsigned long long));
+    p.prof = g_pf_prof;
+  }
   const size_t smem = ring_off() + kRingBytes;
   if (smem > (size_t)kSmemBytes) return mesw_fail(MESW_ERR_UNSUPPORTED, "prefill: shared memory overflow");
   static bool configured = false;
