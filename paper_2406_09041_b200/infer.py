@@ -32,6 +32,7 @@ __all__ = [
     "BatchPlan",
     "ToyBase",
     "batched_multi_model_forward",
+    "batched_greedy_decode",
     "bench_decode",
     "split_bf16",
 ]
@@ -309,7 +310,9 @@ def batched_multi_model_forward(base: ToyBase, registry, plan) -> list:
             for i, (qid, lg, err) in enumerate(res)]
 
 
-def _forward_resident(base: ToyBase, experts: ExpertSet, queries) -> list:
+def _forward_resident(base: ToyBase, experts: ExpertSet, queries, pos0=None) -> list:
+    """pos0[qi]: position of query qi's first token (default 0; decode steps use the last
+    position only -- the toy model has no attention, toylm.py:214-248)."""
     results = {}
     order = []
     for qi, (qid, eid, toks) in enumerate(queries):
@@ -336,7 +339,7 @@ def _forward_resident(base: ToyBase, experts: ExpertSet, queries) -> list:
         else:
             segs.append((cur, cur + toks.size, slot))
         ids.append(toks)
-        pos.append(np.arange(toks.size))
+        pos.append(np.arange(toks.size) + (0 if pos0 is None else int(pos0[qi])))
         cur += toks.size
     if cur:
         all_ids = torch.from_numpy(np.concatenate(ids)).to(dev)
@@ -380,6 +383,62 @@ def _clip_segments(segs, c0: int, c1: int) -> list:
         if b2 < e2:
             out.append((b2 - c0, e2 - c0, s))
     return out
+
+
+def batched_greedy_decode(base: ToyBase, registry, requests) -> list:
+    """Greedy continuation for a batch of requests on the GPU, each with its own expert:
+    requests = [(request id, expert id, prompt token ids, max_new)].  Equal to the reference's
+    greedy_decode(base, providers_e, prompt, max_new) per request (toylm.py:234-248: one
+    position per step, first-maximum argmax); every step is ONE batched multi-expert forward
+    over all still-active requests.  `registry` as in
+    batched_multi_model_forward (experts acquired for the whole decode, released after).
+    Returns [(request id, token ids incl. the prompt, or None, error or None)]."""
+    from .errors import RegistryError
+    reqs = list(requests)
+    own = not isinstance(registry, ExpertSet)
+    experts = registry if not own else ExpertSet(base)
+    acquired, failed = [], {}
+    out = {}
+    try:
+        if own:
+            for eid in dict.fromkeys(r[1] for r in reqs):
+                try:
+                    handle = registry.acquire(eid)
+                except RegistryError as e:
+                    failed[eid] = f"{type(e).__name__}: {e}"
+                    continue
+                acquired.append(eid)
+                experts.add_device(eid, list(handle.layers))
+        seqs = {}
+        for rid, eid, prompt, max_new in reqs:
+            if eid in failed:
+                out[rid] = (rid, None, failed[eid])
+            elif len(prompt) == 0:
+                out[rid] = (rid, None, "empty prompt")
+            else:
+                seqs[rid] = [list(int(t) for t in prompt), int(max_new), eid]
+        step = 0
+        while True:
+            active = [(rid, s) for rid, s in seqs.items() if step < s[1]]  # tokens generated so far = step
+            if not active:
+                break
+            queries = [(rid, s[2], [s[0][-1]]) for rid, s in active]
+            res = _forward_resident(base, experts, queries, pos0=[len(s[0]) - 1 for _, s in active])
+            for (rid, s), (_, logits, err) in zip(active, res):
+                if err is not None:
+                    out[rid] = (rid, None, err)
+                    del seqs[rid]
+                else:
+                    s[0].append(int(np.argmax(logits[-1])))
+            step += 1
+        for rid, s in seqs.items():
+            out[rid] = (rid, s[0], None)
+    finally:
+        if own:
+            stream = torch.cuda.current_stream(base.device)
+            for eid in acquired:
+                registry.release(eid, stream)
+    return [out[r[0]] for r in reqs]
 
 
 # --------------------------------------------------------------------------- bench_decode

@@ -162,10 +162,10 @@ int main() {
   const int R = 4096;
   cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
-  for (int ts : {4, 6})
+  for (int ts : {4, 5})
     for (int cg = 2; cg <= 2; ++cg)
-      for (int nis = 1; nis <= 3; ++nis)
-        for (int N : {16, 48}) {
+      for (int nis = 1; nis <= 1; ++nis)
+        for (int N : {16, 64, 128, 256}) {
           const int cmode = 1;
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3(cg == 2 ? 2 : 1);
