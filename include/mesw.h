@@ -187,6 +187,10 @@ typedef struct {
    * epilogue (~1e-5 relative on the delta term); NULL: exact q expansion.          */
   const float* x_corr;
   int32_t x_corr_ld;
+  /* Optional DEVICE int32 [B]: output (and residual) row of launch row t, -1 = not written.
+   * Lets callers keep their own row order while the launch groups rows by expert
+   * (mesw_pack_x_gather builds the grouped input).  NULL: row t -> row t. */
+  const int32_t* y_rows;
 } mesw_linear_args;
 
 /* ------------------------------------------- K3: prefill fused multi-expert linear
@@ -212,6 +216,11 @@ typedef struct {
 } mesw_prefill_args;
 
 int mesw_me_linear_prefill(const mesw_prefill_args* a, void* stream);
+
+/* mesw_pack_x with a row gather: canonical row t (< rows) = x row d_src[t], or zeros when
+ * d_src[t] < 0 -- groups caller rows by expert on the device (no host round trip). */
+int mesw_pack_x_gather(const uint16_t* d_x, int ldx, const int32_t* d_src, int rows, int m, uint16_t* d_xc,
+                       float* d_corr, int corr_ld, void* stream);
 
 /* Canonical activation layout consumed by mesw_me_linear: rows padded to
  * NP = ceil16(B); for each 128-wide k-step ks a tile of NP*128 bf16 split in two

@@ -37,7 +37,7 @@ class LinearArgs(C.Structure):
                 ("ldy", C.c_int32), ("residual", C.c_void_p), ("ld_res", C.c_int32),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
                 ("counters", C.c_void_p), ("num_ctas", C.c_int32), ("activation", C.c_int32),
-                ("x_corr", C.c_void_p), ("x_corr_ld", C.c_int32)]
+                ("x_corr", C.c_void_p), ("x_corr_ld", C.c_int32), ("y_rows", C.c_void_p)]
 
 
 class PrefillArgs(C.Structure):
@@ -51,6 +51,8 @@ class PrefillArgs(C.Structure):
 _SIGNATURES = [
     ("mesw_abi_version", C.c_int, []),
     ("mesw_me_linear_prefill", C.c_int, [C.POINTER(PrefillArgs), C.c_void_p]),
+    ("mesw_pack_x_gather", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_int, C.c_void_p]),
     ("mesw_last_error", C.c_char_p, []),
     ("mesw_device_sm_count", C.c_int, []),
     ("mesw_set_pdl", C.c_int, [C.c_int]),

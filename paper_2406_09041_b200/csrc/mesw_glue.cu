@@ -447,9 +447,12 @@ __global__ void argmax_kernel(const void* __restrict__ logits, int is_bf16, int 
   }
 }
 
-// Row-major -> canonical (one thread per 16-byte chunk of 8 k); zero padding.
+// Row-major -> canonical (one thread per 16-byte chunk of 8 k); zero padding.  src (optional):
+// canonical row t takes x row src[t] (-1: a zero padding row) -- the expert-grouping gather of
+// the public me_linear path, done on the device.
 __global__ void pack_x_kernel(const uint16_t* __restrict__ x, int B, int m, int ldx, uint16_t* __restrict__ xc,
-                              int NP, int n_ks, float* __restrict__ corr, int corr_ld) {
+                              int NP, int n_ks, float* __restrict__ corr, int corr_ld,
+                              const int32_t* __restrict__ src) {
   pdl_trigger();
   pdl_wait();  // inputs may come from the previous kernel in the stream
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -460,13 +463,14 @@ __global__ void pack_x_kernel(const uint16_t* __restrict__ x, int B, int m, int 
   const int ks = (int)(tid / (16LL * NP));
   const int k0 = ks * 128 + kc * 8;
   uint4 v = make_uint4(0, 0, 0, 0);
-  if (t < B) {
+  const int r = src ? (t < B ? src[t] : -1) : (t < B ? t : -1);
+  if (r >= 0) {
     if (k0 + 8 <= m && (ldx % 8) == 0) {
-      v = *reinterpret_cast<const uint4*>(x + (size_t)t * ldx + k0);
+      v = *reinterpret_cast<const uint4*>(x + (size_t)r * ldx + k0);
     } else {
       uint16_t e[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) e[i] = (k0 + i < m) ? x[(size_t)t * ldx + k0 + i] : (uint16_t)0;
+      for (int i = 0; i < 8; ++i) e[i] = (k0 + i < m) ? x[(size_t)r * ldx + k0 + i] : (uint16_t)0;
       v = make_uint4(e[0] | (uint32_t(e[1]) << 16), e[2] | (uint32_t(e[3]) << 16), e[4] | (uint32_t(e[5]) << 16),
                      e[6] | (uint32_t(e[7]) << 16));
     }
@@ -633,8 +637,19 @@ extern "C" int mesw_pack_x(const uint16_t* d_x, int B, int m, int ldx, uint16_t*
   const long long total = (long long)n_ks * NP * 16;
   if (d_corr && corr_ld < n_ks) return mesw_fail(MESW_ERR_VALUE, "pack_x: corr_ld too small");
   mesw_launch(pack_x_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, d_x, B, m, ldx, d_xc,
-              NP, n_ks, d_corr, corr_ld);
+              NP, n_ks, d_corr, corr_ld, (const int32_t*)nullptr);
   return mesw_check_launch("pack_x");
+}
+
+extern "C" int mesw_pack_x_gather(const uint16_t* d_x, int ldx, const int32_t* d_src, int rows, int m, uint16_t* d_xc,
+                                  float* d_corr, int corr_ld, void* stream) {
+  if (rows <= 0 || m <= 0 || ldx < m || !d_src) return mesw_fail(MESW_ERR_VALUE, "pack_x_gather: bad arguments");
+  const int NP = (rows + 15) & ~15, n_ks = (m + 127) / 128;
+  const long long total = (long long)n_ks * NP * 16;
+  if (d_corr && corr_ld < n_ks) return mesw_fail(MESW_ERR_VALUE, "pack_x_gather: corr_ld too small");
+  mesw_launch(pack_x_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, d_x, rows, m,
+              ldx, d_xc, NP, n_ks, d_corr, corr_ld, d_src);
+  return mesw_check_launch("pack_x_gather");
 }
 
 extern "C" int mesw_unpack_x(const uint16_t* d_xc, int B, int m, uint16_t* d_y, int ldy, void* stream) {

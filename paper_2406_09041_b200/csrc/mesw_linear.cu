@@ -49,7 +49,7 @@ constexpr int kTmemCols = 512;
 #ifndef MESW_DQ_BATCH
 #define MESW_DQ_BATCH 2
 #endif
-constexpr int kDqBatch = MESW_DQ_BATCH;  // jobs per TMEM-store completion wait (see the dequant loop)
+constexpr int kDqBatch = MESW_DQ_BATCH;  // jobs per TMEM-store completion wait (+2 % on C1 at 2)
 // A job = one expert's dequantised A tile for one unit: 128 outputs x 128 k (64 TMEM columns).
 // MESW_HALF_JOBS=1 makes each k-half (32 columns) its own job with its own slot (measured
 // slower: the per-job handshake cost doubles, C1 45 -> 50 us).
@@ -102,6 +102,7 @@ struct LinearParams {
   int a_base[3], a_na[3];
   int ring_bytes;  // dynamic shared memory past the Smem header
   const float* x_corr;  // offset-code bias table [t * x_corr_ld + ks] (OFF kernels)
+  const int32_t* y_rows;  // optional output row map (mesw_linear_args.y_rows)
   int x_corr_ld;
   int n_iss;  // MMA issuer warps (a tcgen05.mma stream runs ~40 cycles/instr per issuer)
   int n_dq;   // delta issuers = active dequant groups (group g feeds delta issuer g)
@@ -120,6 +121,7 @@ struct Smem {
   int flag;
   struct { int on, cg, cgp, p_first, p_last, fast; } fin;  // final-piece reduction hand-off
   int tok2seg[kMaxRows];
+  int yrow[kMaxRows];  // output / residual row of launch row t (-1: not written)
   SegDesc segs[MESW_MAX_SEGMENTS];
   int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
   float xsal[kMaxRows][kSalFast];  // x[t][salient idx r] of the current column group (fast path)
@@ -236,7 +238,8 @@ __device__ __forceinline__ void epi_prefetch(const LinearParams& p, const Smem& 
   }
 #pragma unroll
   for (int t = 0; t < 16; ++t)
-    e.res[t] = (p.residual && t0 + t < p.B && j < p.n) ? bf16_to_f32(p.residual[(size_t)(t0 + t) * p.ld_res + j]) : 0.f;
+    e.res[t] = (p.residual && t0 + t < p.B && j < p.n && S.yrow[t0 + t] >= 0)
+                   ? bf16_to_f32(p.residual[(size_t)S.yrow[t0 + t] * p.ld_res + j]) : 0.f;
 }
 
 // Thread owns output channel j = cg*128 + m; accumulators for the 16 rows [t0, t0+16).
@@ -267,10 +270,12 @@ __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S
     }
     v += e.res[t];
     if (p.activation == 1) v = fmaxf(v, 0.f);
+    const int orow = S.yrow[tok];
+    if (orow < 0) continue;
     if (p.y_bf16)
-      reinterpret_cast<__nv_bfloat16*>(p.y)[(size_t)tok * p.ldy + j] = __float2bfloat16_rn(v);
+      reinterpret_cast<__nv_bfloat16*>(p.y)[(size_t)orow * p.ldy + j] = __float2bfloat16_rn(v);
     else
-      reinterpret_cast<float*>(p.y)[(size_t)tok * p.ldy + j] = v;
+      reinterpret_cast<float*>(p.y)[(size_t)orow * p.ldy + j] = v;
   }
 }
 
@@ -366,7 +371,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
                  "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
-  for (int i = threadIdx.x; i < kMaxRows; i += kThreads) S.tok2seg[i] = -1;
+  for (int i = threadIdx.x; i < kMaxRows; i += kThreads) {
+    S.tok2seg[i] = -1;
+    S.yrow[i] = i < p.B ? (p.y_rows ? p.y_rows[i] : i) : -1;  // written by the host before launch
+  }
   if (threadIdx.x == 0) S.fin.on = 0;
   __syncthreads();
   for (int q = threadIdx.x; q < p.n_seg; q += kThreads) {
@@ -985,6 +993,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
     p.seg_begin[s] = a->seg_begin[s]; p.seg_end[s] = a->seg_end[s]; p.seg_slot[s] = a->seg_slot[s];
   }
   p.y = a->y; p.y_bf16 = a->y_bf16; p.ldy = a->ldy;
+  p.y_rows = a->y_rows;
   p.residual = a->residual; p.ld_res = a->ld_res;
   p.ws = reinterpret_cast<float*>(a->workspace);
   p.counters = a->counters;

@@ -620,6 +620,51 @@ def align_segments(B: int, segments) -> tuple:
     return len(src), new_segs, src
 
 
+_ME_PLANS: dict = {}
+_ME_PLANS_MAX = 64
+
+
+class _MeLinearPlan:
+    """Cached device state of one me_linear call shape: row gather indices, canonical input
+    and bias-table buffers and the bound launch plan(s) -- per call only the gather-pack and
+    the fused launch run (two kernels, no host-side tensor ops)."""
+
+    def __init__(self, x, weight, table, segs, out, residual, geom, num_ctas, activation, offset_codes):
+        B = x.shape[0]
+        dev = x.device
+        rows, new_segs, src = align_segments(B, segs)
+        self.launches = []
+        start = 0
+        while start < rows:
+            end = min(rows, start + MAX_ROWS)
+            n_rows = end - start
+            csegs = [(max(b, start) - start, min(e, end) - start, sl) for b, e, sl in new_segs if b < end and e > start]
+            src_t = torch.as_tensor(src[start:end], dtype=torch.int32, device=dev)
+            xc = torch.empty(canonical_numel(n_rows, geom.m), dtype=torch.bfloat16, device=dev)
+            corr = corr_table(n_rows, geom.m, dev) if (offset_codes and csegs) else None
+            plan = None
+            if weight is not None or csegs:
+                plan = LinearPlan(xc, n_rows, weight, table if csegs else None, csegs, out, residual, geom,
+                                  num_ctas, activation, x_corr=corr)
+                plan.args.y_rows = src_t.data_ptr()  # grouped launch row -> caller's row (or -1)
+            self.launches.append((src_t, n_rows, xc, corr, plan))
+            start = end
+        self.keep = (weight, table)  # identity-checked by me_linear (ids alone could be reused)
+
+    def __call__(self, x, out, residual, stream=None):
+        L = _lib.lib()
+        s = _stream(stream)
+        for src_t, n_rows, xc, corr, plan in self.launches:
+            if plan is None:
+                continue
+            plan.args.y = out.data_ptr()  # per-call tensors: rebinding two pointers is all it takes
+            plan.args.residual = residual.data_ptr() if residual is not None else None
+            _lib.check(L.mesw_pack_x_gather(x.data_ptr(), x.stride(0), src_t.data_ptr(), n_rows, plan.geom.m,
+                                            xc.data_ptr(), corr.data_ptr() if corr is not None else None,
+                                            corr.stride(0) if corr is not None else 0, s))
+            plan(stream)
+
+
 def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
               segments, out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
               out_dtype=torch.bfloat16, geom: LinearGeometry | None = None, num_ctas: int = 0,
@@ -630,50 +675,39 @@ def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable |
     (mesw.h x_corr; the bf16 serving engine's choice, ~1e-5 relative on the delta term).
     The default keeps the exact q expansion (the f32 provider path holds 1e-4).
 
-    x: bf16 [B, >= m] on the GPU, rows grouped by expert; segments: iterable of
-    (begin, end, slot) into `table`.  The rows are packed into the canonical layout;
-    segments not starting on a 16-row boundary are re-laid out (rows are independent,
-    so results equal those of the caller's layout) and batches beyond the per-launch
-    row budget are split.
+    x: bf16 [B, >= m] on the GPU (row-contiguous), rows in any order; segments: iterable of
+    (begin, end, slot) into `table`.  The device gathers the rows into expert groups on
+    16-row boundaries (mesw_pack_x_gather) and the kernel's epilogue writes every result
+    straight back to the caller's row (mesw_linear_args.y_rows): no host-side gathers or
+    scatters, and the launch state is cached per call shape (one pack + one fused launch
+    per <= 192 grouped rows).  Rows in no segment get the base term only.
     """
     if geom is None:
         geom = weight.geom if weight is not None else next(
             d.geom for d in table.deltas if d is not None)
+    if x.dtype != torch.bfloat16 or not x.is_cuda or x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("x must be a row-contiguous 2-D bf16 CUDA tensor")
+    if x.shape[1] < geom.m:
+        raise ValueError(f"x has {x.shape[1]} columns, the linear needs {geom.m}")
     B = x.shape[0]
     if out is None:
         out = torch.empty((B, geom.n), dtype=out_dtype, device=x.device)
-    segs = [(int(b), int(e), int(s)) for b, e, s in segments]
-    xm = x[:, :geom.m] if x.shape[1] >= geom.m else x
-    if all(b % 16 == 0 for b, _, _ in segs) and B <= MAX_ROWS:
-        corr = corr_table(B, geom.m, x.device) if offset_codes else None
-        xc = pack_x(xm.contiguous() if xm.stride(1) != 1 else xm, stream=stream, corr=corr)
-        LinearPlan(xc, B, weight, table, segs, out, residual, geom, num_ctas, activation, x_corr=corr)(stream)
+    segs = tuple((int(b), int(e), int(s)) for b, e, s in segments)
+    if weight is None and not segs:
+        out.zero_()
         return out
-    rows, new_segs, src = align_segments(B, segs)
-    cuts, start = [], 0
-    while start < rows:
-        end = min(rows, start + MAX_ROWS)
-        cuts.append((start, end))
-        start = end
-    src_all = torch.as_tensor(src, dtype=torch.int64, device=x.device)
-    for c0, c1 in cuts:
-        src_t = src_all[c0:c1]
-        valid = src_t >= 0
-        n_rows = c1 - c0
-        csegs = [(max(b, c0) - c0, min(e, c1) - c0, sl) for b, e, sl in new_segs if b < c1 and e > c0]
-        xp = torch.zeros((n_rows, geom.m), dtype=x.dtype, device=x.device)
-        xp[valid] = xm[src_t[valid]]
-        rp = None
-        if residual is not None:
-            rp = torch.zeros((n_rows, residual.shape[1]), dtype=residual.dtype, device=x.device)
-            rp[valid] = residual[src_t[valid]]
-        yp = torch.empty((n_rows, out.shape[1]), dtype=out.dtype, device=x.device)
-        if weight is None and not csegs:
-            yp.zero_()
-        else:
-            corr = corr_table(n_rows, geom.m, x.device) if offset_codes else None
-            xc = pack_x(xp, stream=stream, corr=corr)
-            LinearPlan(xc, n_rows, weight, table if csegs else None, csegs, yp, rp, geom, num_ctas,
-                       activation, x_corr=corr)(stream)
-        out[src_t[valid]] = yp[valid]
+    if out.shape[0] < B or out.stride(1) != 1 or out.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("out must be a row-contiguous bf16/f32 tensor with >= B rows")
+    if residual is not None and (residual.dtype != torch.bfloat16 or residual.stride(1) != 1):
+        raise ValueError("residual must be a row-contiguous bf16 tensor")
+    key = (x.device, tuple(x.shape), x.stride(0), id(weight), id(table), segs, out.dtype, out.stride(0),
+           residual.stride(0) if residual is not None else None, geom, num_ctas, activation, bool(offset_codes),
+           table.dev.data_ptr() if table is not None else None)
+    plan = _ME_PLANS.get(key)
+    if plan is None or plan.keep[0] is not weight or plan.keep[1] is not table:
+        if len(_ME_PLANS) >= _ME_PLANS_MAX:
+            _ME_PLANS.pop(next(iter(_ME_PLANS)))
+        plan = _MeLinearPlan(x, weight, table, segs, out, residual, geom, num_ctas, activation, offset_codes)
+        _ME_PLANS[key] = plan
+    plan(x, out, residual, stream)
     return out

@@ -258,3 +258,38 @@ def test_pack_x_roundtrip_and_layout():
         idx = ((k // 128) * NP * 128 + ((t // 8) % 2) * (NP // 2) * 128 + (t // 16) * 1024
                + ((k % 128) // 8) * 64 + (t % 8) * 8 + k % 8)
         assert flat[idx] == x[t, k].cpu()
+
+
+def test_me_linear_caller_row_order_on_device():
+    """Public me_linear with rows in arbitrary order (experts interleaved, base-only rows,
+    residual): rows are grouped on the device (mesw_pack_x_gather) and results written back
+    to the caller's rows by the epilogue (y_rows) -- bitwise equal to calling the kernel on
+    pre-grouped rows, and the call issues only libmesw kernels."""
+    import torch
+    from paper_2406_09041_b200 import compress
+    from paper_2406_09041_b200.device import DeviceDelta, DeviceWeight, ExpertTable, me_linear
+    rng = np.random.default_rng(21)
+    m, n = 256, 384
+    W = rng.normal(0, 0.02, size=(m, n)).astype(np.float32)
+    dw = DeviceWeight.from_dense([W])
+    table = ExpertTable("cuda")
+    man = {"model_id": "x", "domain": "d", "base_digest": "0", "layer_count": 1}
+    for e in range(3):
+        ol = om.random_layer(rng, m, n, 2, 8)
+        table.set(e, DeviceDelta.from_blocks([compress.deserialize_artifact(om.serialize_artifact(man, [ol])).layers[0]]))
+    B = 23
+    x = torch.from_numpy(rng.normal(0, 1, size=(B, m)).astype(np.float32)).to(torch.bfloat16).cuda()
+    res = torch.from_numpy(rng.normal(0, 1, size=(B, n)).astype(np.float32)).to(torch.bfloat16).cuda()
+    segs = [(0, 5, 2), (5, 6, 0), (6, 17, 1)]  # rows 17..22: base only
+    y1 = me_linear(x, dw, table, segs, residual=res, out_dtype=torch.float32)
+    y2 = me_linear(x, dw, table, segs, residual=res, out_dtype=torch.float32)  # cached plan
+    # reference launch: the same rows pre-grouped on 16-row boundaries, one segment per window
+    order = list(range(0, 5)) + [-1] * 11 + [5] + [-1] * 15 + list(range(6, 17)) + [-1] * 5 + list(range(17, 23))
+    xg = torch.zeros((len(order), m), dtype=torch.bfloat16, device="cuda")
+    rg = torch.zeros((len(order), n), dtype=torch.bfloat16, device="cuda")
+    for i, r in enumerate(order):
+        if r >= 0:
+            xg[i], rg[i] = x[r], res[r]
+    yg = me_linear(xg, dw, table, [(0, 5, 2), (16, 17, 0), (32, 43, 1)], residual=rg, out_dtype=torch.float32)
+    want = torch.stack([yg[order.index(r)] for r in range(B)])
+    assert torch.equal(y1, want) and torch.equal(y2, want)
