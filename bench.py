@@ -127,6 +127,11 @@ def main():
         from bench_impl import reference_arm
         if rank != 0:
             return 0
+        try:  # torchrun sets OMP_NUM_THREADS=1 per rank; the reference arm is rank 0 alone: use all cores
+            from threadpoolctl import threadpool_limits
+            threadpool_limits(os.cpu_count())
+        except Exception:
+            pass
         line = reference_arm(args)
         print(json.dumps(line), flush=True)
         return 0

@@ -88,7 +88,9 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __
 #define MESW_NORM_THREADS 256
 #endif
 constexpr int kNormThreads = MESW_NORM_THREADS;
-constexpr int kNormMaxVec = 2048 / MESW_NORM_THREADS;  // up to 8192 channels
+// 16-byte vectors per thread: 8192 channels = 1024 vectors of 8 over the block
+constexpr int kNormMaxVec = 1024 / MESW_NORM_THREADS;
+static_assert(1024 % MESW_NORM_THREADS == 0, "MESW_NORM_THREADS must divide 1024");
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const uint16_t* __restrict__ x, int ldx,
                                                                const uint16_t* __restrict__ w, int H, float eps,
                                                                uint16_t* __restrict__ y, int ldy, int ynp,
