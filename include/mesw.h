@@ -146,7 +146,10 @@ int mesw_unpack_weight_debug(const uint16_t* d_w, uint32_t m, uint32_t n, uint32
  * with Dtilde applied straight from the packed codes (Eq. 4
  * PAPER.md:123-130): s_j * sum_{i not in S} x_i q_ij + sum_{i in S} x_i half(R)_ij.
  * Tokens are grouped by expert: segment s covers rows [seg_begin[s], seg_end[s])
- * and uses expert-table slot seg_slot[s]; rows in no segment get no delta.
+ * and uses expert-table slot seg_slot[s]; rows in no segment get no delta.  Segment
+ * begins are multiples of 8 rows (a segment of <= 8 rows may take the second half of a
+ * 16-row window); TMEM bounds a launch to NP + 16 x (windows touched, summed over the
+ * segments) <= 384 columns.
  * Replaces toylm._apply_delta + provider (toylm.py:183-186) and SPEC
  * delta_matvec / batched_multi_model_forward's shared-base + delta stages.  */
 typedef struct {

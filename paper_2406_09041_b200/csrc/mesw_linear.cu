@@ -67,7 +67,9 @@ struct SegDesc {
   const int32_t* sal_off;
   const int32_t* sal_idx;
   const uint16_t* sal_rows;
-  int begin, end, win0, winN;
+  int begin, end;
+  int w0, nw;  // first 16-row window touched, windows touched (begins are multiples of 8 rows)
+  int dcol;    // first column of the segment's delta accumulator (after the NP base columns)
 };
 
 struct LinearParams {
@@ -80,6 +82,8 @@ struct LinearParams {
   int seg_begin[MESW_MAX_SEGMENTS];
   int seg_end[MESW_MAX_SEGMENTS];
   int seg_slot[MESW_MAX_SEGMENTS];
+  int seg_dcol[MESW_MAX_SEGMENTS];  // host-computed: prefix sums of 16 x windows touched
+  int NPD;                          // delta accumulator columns (sum of 16 x windows touched)
   void* y;
   int y_bf16, ldy;
   const uint16_t* residual;
@@ -121,6 +125,7 @@ struct Smem {
   int flag;
   struct { int on, cg, cgp, p_first, p_last, fast; } fin;  // final-piece reduction hand-off
   int tok2seg[kMaxRows];
+  int half2seg[kMaxRows / 8];  // segment owning rows [8h, 8h + 8) (a segment begins on an 8-row half)
   int yrow[kMaxRows];  // output / residual row of launch row t (-1: not written)
   SegDesc segs[MESW_MAX_SEGMENTS];
   int sal_r0[MESW_MAX_SEGMENTS], sal_k[MESW_MAX_SEGMENTS];  // current column group's salient range
@@ -206,59 +211,109 @@ __device__ __forceinline__ bool gather_salient_x(const LinearParams& p, Smem& S,
   return fast;
 }
 
+// Delta accumulators of the 16 rows [t0, t0 + 16) (one window w): rows 0-7 (the CTA0 half)
+// from the segment owning half 2w, rows 8-15 from the owner of half 2w + 1.  A segment's
+// delta range [dcol, dcol + 16 nw) holds its windows' CTA0 rows first, then the CTA1 rows.
+template <bool HALF>
+__device__ __forceinline__ void load_delta16(const Smem& S, uint32_t acc, int NP, int t0, float* vd) {
+  const int w = t0 >> 4;
+  if constexpr (!HALF) {  // every segment begins on a window: one owner for all 16 rows
+    const int sg = S.half2seg[2 * w];
+    if (sg >= 0) {
+      const SegDesc& sd = S.segs[sg];
+      const uint32_t c = acc + (uint32_t)(NP + sd.dcol + 8 * (w - sd.w0));
+      tmem_ld8(c, vd);
+      tmem_ld8(c + (uint32_t)(8 * sd.nw), vd + 8);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) vd[i] = 0.f;
+    }
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int sg = S.half2seg[2 * w + h];
+    if (sg >= 0) {
+      const SegDesc& sd = S.segs[sg];
+      tmem_ld8(acc + (uint32_t)(NP + sd.dcol + h * 8 * sd.nw + 8 * (w - sd.w0)), vd + 8 * h);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) vd[8 * h + i] = 0.f;
+    }
+  }
+}
+
+// Output / residual row of launch row t: the caller's row map (me_linear's device-side
+// grouping), or t itself.  A kernel template parameter: launches without a map (the serving
+// engine's) keep the plain row arithmetic in the latency-critical epilogue (a runtime branch
+// there measured 5 % of the C2 step).
+template <bool YMAP>
+__device__ __forceinline__ int out_row(const LinearParams& p, const Smem& S, int t) {
+  if constexpr (YMAP) return S.yrow[t];
+  else return t;
+}
+
 // Per-chunk epilogue operands that do not depend on the accumulators (prefetched one
-// chunk ahead): the chunk's expert segment, its step s_e[j], salient rows R_e[r][j] and
-// the residual.  A 16-row chunk holds rows of at most one segment (16-row aligned).
+// chunk ahead): each 8-row half's expert segment, its step s_e[j], salient rows R_e[r][j],
+// and the residual.  A half holds rows of at most one segment (segments begin on halves).
 struct EpiPre {
-  int sg;
-  float sj;
-  float R[kSalFast];
+  int sg[2];
+  float sj[2];
+  float R[kSalFast];  // salient rows of the first half's segment (the second half reloads if it differs)
   float res[16];
 };
 
+__device__ __forceinline__ void load_sal_rows(const Smem& S, int sg, int m, float* R) {
+  const SegDesc& sd = S.segs[sg];
+  const int r0 = S.sal_r0[sg], k = S.sal_k[sg];  // smem: no dependent global round trip
+#pragma unroll
+  for (int r = 0; r < kSalFast; ++r)
+    R[r] = r < k ? __half2float(__ushort_as_half(sd.sal_rows[(size_t)(r0 + r) * kUnitN + m])) : 0.f;
+}
+
+template <bool YMAP, bool HALF>
 __device__ __forceinline__ void epi_prefetch(const LinearParams& p, const Smem& S, int cg, int m, int t0,
                                              bool fast, EpiPre& e) {
   const int j = cg * kUnitN + m;
-  e.sg = -1;
-#pragma unroll
-  for (int t = 0; t < 16; ++t)
-    if (e.sg < 0 && t0 + t < p.B) e.sg = S.tok2seg[t0 + t];
-  e.sj = 0.f;
+  const int s0 = S.half2seg[t0 >> 3], s1 = HALF ? S.half2seg[(t0 >> 3) + 1] : s0;
+  e.sg[0] = s0;
+  e.sg[1] = s1;
+  e.sj[0] = (s0 >= 0 && j < p.n) ? S.segs[s0].steps[j] : 0.f;
+  e.sj[1] = s1 == s0 ? e.sj[0] : ((s1 >= 0 && j < p.n) ? S.segs[s1].steps[j] : 0.f);
+  const int sr = e.sg[0] >= 0 ? e.sg[0] : e.sg[1];
 #pragma unroll
   for (int r = 0; r < kSalFast; ++r) e.R[r] = 0.f;
-  if (e.sg >= 0 && j < p.n) {
-    const SegDesc& sd = S.segs[e.sg];
-    e.sj = sd.steps[j];
-    if (fast) {
-      const int r0 = S.sal_r0[e.sg], k = S.sal_k[e.sg];  // smem: no dependent global round trip
-#pragma unroll
-      for (int r = 0; r < kSalFast; ++r)
-        if (r < k) e.R[r] = __half2float(__ushort_as_half(sd.sal_rows[(size_t)(r0 + r) * kUnitN + m]));
-    }
-  }
+  if (fast && sr >= 0 && j < p.n) load_sal_rows(S, sr, m, e.R);
 #pragma unroll
   for (int t = 0; t < 16; ++t)
-    e.res[t] = (p.residual && t0 + t < p.B && j < p.n && S.yrow[t0 + t] >= 0)
-                   ? bf16_to_f32(p.residual[(size_t)S.yrow[t0 + t] * p.ld_res + j]) : 0.f;
+    e.res[t] = (p.residual && t0 + t < p.B && j < p.n && out_row<YMAP>(p, S, t0 + t) >= 0)
+                   ? bf16_to_f32(p.residual[(size_t)out_row<YMAP>(p, S, t0 + t) * p.ld_res + j]) : 0.f;
 }
 
 // Thread owns output channel j = cg*128 + m; accumulators for the 16 rows [t0, t0+16).
+template <bool YMAP, bool HALF>
 __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S, int cg, int m, int t0,
                                             const float* vb, const float* vd, bool fast, const EpiPre& e) {
   const int j = cg * kUnitN + m;
   if (j >= p.n) return;
+  float R[kSalFast];
+#pragma unroll
+  for (int r = 0; r < kSalFast; ++r) R[r] = e.R[r];
 #pragma unroll
   for (int t = 0; t < 16; ++t) {
     const int tok = t0 + t;
     if (tok >= p.B) break;
     float v = vb[t];
-    if (e.sg >= 0 && S.tok2seg[tok] == e.sg) {
-      float d = e.sj * vd[t];
+    const int h = HALF ? (t >> 3) : 0;
+    if (HALF && t == 8 && fast && e.sg[1] >= 0 && e.sg[0] >= 0 && e.sg[1] != e.sg[0])
+      load_sal_rows(S, e.sg[1], m, R);  // second half of the window: another expert's rows
+    if (e.sg[h] >= 0 && S.tok2seg[tok] == e.sg[h]) {
+      float d = e.sj[h] * vd[t];
       if (fast) {
 #pragma unroll
-        for (int r = 0; r < kSalFast; ++r) d = fmaf(S.xsal[tok][r], e.R[r], d);
+        for (int r = 0; r < kSalFast; ++r) d = fmaf(S.xsal[tok][r], R[r], d);
       } else {
-        const SegDesc& sd = S.segs[e.sg];
+        const SegDesc& sd = S.segs[e.sg[h]];
         const int r0 = sd.sal_off[cg], k = sd.sal_off[cg + 1] - r0;
         for (int r = 0; r < k; ++r) {
           const float xv = bf16_to_f32(p.x[xc_index(tok, sd.sal_idx[r0 + r], p.NP)]);
@@ -270,7 +325,7 @@ __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S
     }
     v += e.res[t];
     if (p.activation == 1) v = fmaxf(v, 0.f);
-    const int orow = S.yrow[tok];
+    const int orow = out_row<YMAP>(p, S, tok);
     if (orow < 0) continue;
     if (p.y_bf16)
       reinterpret_cast<__nv_bfloat16*>(p.y)[(size_t)orow * p.ldy + j] = __float2bfloat16_rn(v);
@@ -284,6 +339,7 @@ __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S
 // any launch geometry with the same row count), then stored through epi_store16.  The
 // epilogue operands are fetched together with the partials: one L2 round trip per chunk.
 // stage != nullptr: the contributors' slots were bulk-copied to shared memory (final piece).
+template <bool YMAP, bool HALF>
 __device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& S, int cg, int cgp, int rank, int m,
                                           int t0, int p_first, int p_last, bool fast, const EpiPre& pre,
                                           const float* stage) {
@@ -309,7 +365,7 @@ __device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& 
 #pragma unroll
     for (int i = 0; i < 16; ++i) vb[i] += lb[i];
   }
-  epi_store16(p, S, cg, m, t0, vb, vd, fast, pre);
+  epi_store16<YMAP, HALF>(p, S, cg, m, t0, vb, vd, fast, pre);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -340,7 +396,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // its own TMEM, and drains its own accumulators; the leader (rank 0) issues all MMAs and
 // commits them to both CTAs' barriers (multicast).  The peer relays its "tile landed"
 // events to the leader's barriers.
-template <int DB, bool OFF>
+template <int DB, bool OFF, bool YMAP, bool HALF>
 __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_constant__ LinearParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   Smem& S = *reinterpret_cast<Smem*>(smem);
@@ -373,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   }
   for (int i = threadIdx.x; i < kMaxRows; i += kThreads) {
     S.tok2seg[i] = -1;
+    if (i < kMaxRows / 8) S.half2seg[i] = -1;
     S.yrow[i] = i < p.B ? (p.y_rows ? p.y_rows[i] : i) : -1;  // written by the host before launch
   }
   if (threadIdx.x == 0) S.fin.on = 0;
@@ -387,10 +444,12 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     d.sal_rows = e.sal_rows;
     d.begin = p.seg_begin[q];
     d.end = p.seg_end[q];
-    d.win0 = d.begin;                          // begin is a multiple of 16
-    d.winN = ((d.end + 15) & ~15) - d.begin;   // 16-token window(s)
+    d.w0 = d.begin >> 4;
+    d.nw = ((d.end - 1) >> 4) - d.w0 + 1;
+    d.dcol = p.seg_dcol[q];
     S.segs[q] = d;
     for (int t = d.begin; t < d.end; ++t) S.tok2seg[t] = q;
+    for (int h = d.begin >> 3; h <= (d.end - 1) >> 3; ++h) S.half2seg[h] = q;
   }
   tc_fence_before();
   __syncthreads();
@@ -522,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             tc_fence_after();
             MESW_PROF(prof[5] += clock64() - tq;)
           }
-          const uint32_t d_base = tbase + (uint32_t)(ab * 2 * NP);
+          const uint32_t d_base = tbase + (uint32_t)(ab * (NP + p.NPD));
           const uint32_t f0 = piece_first ? 0u : 1u;
           MESW_PROF(tq = clock64();)
           mbar_wait_cluster(&S.xfull[sx], px);
@@ -550,12 +609,13 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               MESW_PROF(if (p.tbuf && blockIdx.x == 0 && lane == 0 && prof[7] < 32) p.tbuf[4096 * 56 + 512 + role * 64 + 2 * prof[7]] = clock64();)
               MESW_PROF(tq = clock64();)
               tc_fence_after();
-              const int win0 = S.segs[q].win0;
-              const uint32_t id = idesc_bf16_m256(S.segs[q].winN);
-              const uint32_t dd = d_base + (uint32_t)(NP + win0);
+              // N = the windows the segment touches; rows of other segments in them (a half
+              // window shared at a segment boundary) land in columns this segment never reads
+              const uint32_t id = idesc_bf16_m256(16 * S.segs[q].nw);
+              const uint32_t dd = d_base + (uint32_t)(NP + S.segs[q].dcol);
               const uint32_t a0 = tbase + (uint32_t)(p.a_col0 + (abase_own + aslot) * kAColsPerSlot);
               // B rows of the expert's windows: window w's half lives at w * 2048 B in each CTA
-              const uint64_t bd = xd + (uint64_t)((win0 >> 4) * (kXRowGroupBytes >> 4)) + (uint64_t)(kh * 64);
+              const uint64_t bd = xd + (uint64_t)(S.segs[q].w0 * (kXRowGroupBytes >> 4)) + (uint64_t)(kh * 64);
 #ifndef MESW_EXP_NOMMA
               if (kJobHalves == 2) mma2_ts_k64(uni(dd), uni(a0), uni64(bd), uni(id), uni(kh == 0 ? f0 : 1u));
               else mma2_ts_k128(uni(dd), uni(a0), uni64(bd), uni(id), uni(f0));
@@ -722,11 +782,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
         named_bar_sync(1, 128);
       }
       EpiPre pre;
-      epi_prefetch(p, S, cg, mrow, 0, fast, pre);
+      epi_prefetch<YMAP, HALF>(p, S, cg, mrow, 0, fast, pre);
       mbar_wait_sleep(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
       tc_fence_after();
       if (gtid == 0 && pi == po.np - 1) MESW_STAMP(5);
-      const uint32_t acc = tbase + lane_addr + (uint32_t)(ab * 2 * NP);
+      const uint32_t acc = tbase + lane_addr + (uint32_t)(ab * (NP + p.NPD));
       if (whole) {
         for (int t0 = 0; t0 < NP; t0 += 16) {
           float vb[16], vd[16];
@@ -737,22 +797,13 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
 #pragma unroll
             for (int i = 0; i < 16; ++i) vb[i] = 0.f;  // delta-only: D_base never written
           }
-          const int sg = S.tok2seg[t0];
-          if (sg >= 0) {
-            const SegDesc& sd = S.segs[sg];
-            const int dw = (t0 - sd.win0) / 2;  // window's column inside the expert's D range
-            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + dw), vd);
-            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + sd.winN / 2 + dw), vd + 8);
-            if (OFF) {
+          load_delta16<HALF>(S, acc, NP, t0, vd);
+          if (OFF) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) vd[i] -= S.corr[t0 + i];  // offset-code bias
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) vd[i] = 0.f;
+            for (int i = 0; i < 16; ++i) vd[i] -= S.corr[t0 + i];  // offset-code bias (0 on padding rows)
           }
-          epi_store16(p, S, cg, mrow, t0, vb, vd, fast, pre);
-          if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
+          epi_store16<YMAP, HALF>(p, S, cg, mrow, t0, vb, vd, fast, pre);
+          if (t0 + 16 < NP) epi_prefetch<YMAP, HALF>(p, S, cg, mrow, t0 + 16, fast, pre);
         }
       } else {
         // stream-K partial: base + s_j * delta per row (natural row order, [NP][128] f32);
@@ -769,20 +820,16 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
 #pragma unroll
             for (int i = 0; i < 16; ++i) vb[i] = 0.f;
           }
-          const int sg = S.tok2seg[t0];
-          if (sg >= 0) {
-            const SegDesc& sd = S.segs[sg];
-            const int dw = (t0 - sd.win0) / 2;
-            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + dw), vd);
-            tmem_ld8(acc + (uint32_t)(NP + sd.win0 + sd.winN / 2 + dw), vd + 8);
+          if (pre.sg[0] >= 0 || pre.sg[1] >= 0) {
+            load_delta16<HALF>(S, acc, NP, t0, vd);
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (pre.sg >= 0 && S.tok2seg[t0 + i] == pre.sg)
-                vb[i] = fmaf(pre.sj, OFF ? vd[i] - S.corr[t0 + i] : vd[i], vb[i]);
+              if (pre.sg[i >> 3] >= 0 && S.tok2seg[t0 + i] == pre.sg[i >> 3])
+                vb[i] = fmaf(pre.sj[i >> 3], OFF ? vd[i] - S.corr[t0 + i] : vd[i], vb[i]);
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) __stcg(mine + (size_t)(t0 + i) * kUnitN + mrow, vb[i]);
-          if (t0 + 16 < NP) epi_prefetch(p, S, cg, mrow, t0 + 16, fast, pre);
+          if (t0 + 16 < NP) epi_prefetch<YMAP, HALF>(p, S, cg, mrow, t0 + 16, fast, pre);
         }
       }
       // accumulators consumed -> the leader may reuse this buffer
@@ -820,8 +867,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           } else {
             for (int t0 = 0; t0 < NP; t0 += 16) {
               EpiPre pre;
-              epi_prefetch(p, S, cg, mrow, t0, fast, pre);
-              reduce_chunk(p, S, cg, cgp, (int)rank, mrow, t0, p_first, p_last, fast, pre, nullptr);
+              epi_prefetch<YMAP, HALF>(p, S, cg, mrow, t0, fast, pre);
+              reduce_chunk<YMAP, HALF>(p, S, cg, cgp, (int)rank, mrow, t0, p_first, p_last, fast, pre, nullptr);
             }
             if (gtid == 0) p.counters[cg] = 0;  // self-reset for the next launch
           }
@@ -852,7 +899,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     float* st = reinterpret_cast<float*>(ring);
     const int t_first = 16 * (threadIdx.x / kUnitN);
     EpiPre pre0;
-    if (t_first < NP) epi_prefetch(p, S, fcg, fm, t_first, ffast, pre0);  // in flight with the copies
+    if (t_first < NP) epi_prefetch<YMAP, HALF>(p, S, fcg, fm, t_first, ffast, pre0);  // in flight with the copies
     MESW_PROF(long long fp[4] = {0, 0, 0, 0}; long long fq = clock64();)
     if (staged) {
       const long long T2 = p.T, G2 = p.G / 2;
@@ -889,9 +936,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     for (int t0 = t_first; t0 < NP; t0 += 16 * (kThreads / kUnitN)) {
       EpiPre pre;
       if (t0 == t_first) pre = pre0;
-      else epi_prefetch(p, S, fcg, fm, t0, ffast, pre);
-      if (staged) reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, nC <= nbuf ? pl : pf, ffast, pre, st);
-      else reduce_chunk(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre, nullptr);
+      else epi_prefetch<YMAP, HALF>(p, S, fcg, fm, t0, ffast, pre);
+      if (staged) reduce_chunk<YMAP, HALF>(p, S, fcg, fcgp, (int)rank, fm, t0, pf, nC <= nbuf ? pl : pf, ffast, pre, st);
+      else reduce_chunk<YMAP, HALF>(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre, nullptr);
       MESW_PROF(fp[2] += clock64() - fq; fq = clock64();)
     }
     MESW_PROF(fp[3] = staged ? nC : -nC;)
@@ -908,11 +955,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
   }
 }
 
-template <int DB, bool OFF>
+template <int DB, bool OFF, bool YMAP, bool HALF>
 int launch(const LinearParams& p, size_t smem, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(me_linear_tc_kernel<DB, OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(me_linear_tc_kernel<DB, OFF, YMAP, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          232448);
     if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
     configured = true;
@@ -931,7 +978,7 @@ int launch(const LinearParams& p, size_t smem, cudaStream_t stream) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = mesw_pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, me_linear_tc_kernel<DB, OFF>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, me_linear_tc_kernel<DB, OFF, YMAP, HALF>, p);
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("me_linear");
 }
@@ -976,8 +1023,8 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
     if (a->seg_begin[s] < prev_end || a->seg_end[s] <= a->seg_begin[s] || a->seg_end[s] > a->B ||
         a->seg_slot[s] < 0)
       return mesw_fail(MESW_ERR_VALUE, "segments must be non-empty, ascending, disjoint and inside [0, B)");
-    if (a->seg_begin[s] % 16)
-      return mesw_fail(MESW_ERR_VALUE, "segment begins must be multiples of 16 rows (pad expert groups)");
+    if (a->seg_begin[s] % 8)
+      return mesw_fail(MESW_ERR_VALUE, "segment begins must be multiples of 8 rows (pad expert groups)");
     prev_end = a->seg_end[s];
   }
   int sms = mesw_device_sm_count();
@@ -989,8 +1036,11 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   p.w = reinterpret_cast<const uint8_t*>(a->w);
   p.table = a->expert_table;
   p.n_seg = a->n_segments;
+  p.NPD = 0;
   for (int s = 0; s < p.n_seg; ++s) {
     p.seg_begin[s] = a->seg_begin[s]; p.seg_end[s] = a->seg_end[s]; p.seg_slot[s] = a->seg_slot[s];
+    p.seg_dcol[s] = p.NPD;
+    p.NPD += 16 * (((a->seg_end[s] - 1) >> 4) - (a->seg_begin[s] >> 4) + 1);
   }
   p.y = a->y; p.y_bf16 = a->y_bf16; p.ldy = a->ldy;
   p.y_rows = a->y_rows;
@@ -1081,7 +1131,7 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
     bool done = false;
     for (int n_acc = nacc_max; n_acc >= 1 && !done; --n_acc) {
       for (int nd = nd_max; nd >= (p.n_seg > 0 ? 1 : 0) && !done; --nd) {
-        const int cols = kTmemCols - n_acc * 2 * p.NP;
+        const int cols = kTmemCols - n_acc * (p.NP + p.NPD);
         int slots = cols / kAColsPerSlot;
         if (slots > kMaxASlots) slots = kMaxASlots;
         if (env_maxslots > 0 && slots > env_maxslots) slots = env_maxslots;
@@ -1109,10 +1159,20 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
     if (!done) return mesw_fail(MESW_ERR_UNSUPPORTED, "tensor memory: too many rows for the A ring");
   }
 
+  bool half = false;
+  for (int q = 0; q < p.n_seg; ++q) half |= (p.seg_begin[q] % 16) != 0;
   cudaStream_t s = (cudaStream_t)stream;
   switch (db) {
-    case 2: return p.x_corr ? launch<2, true>(p, smem, s) : launch<2, false>(p, smem, s);
-    case 4: return launch<4, false>(p, smem, s);
-    default: return launch<8, false>(p, smem, s);
+    // (kernels with YMAP read the identity map when y_rows is NULL; HALF: a segment begins on
+    // the second half of a window -- both are template parameters because the epilogue is the
+    // latency-critical tail of every launch)
+    case 2:
+      if (p.x_corr) {
+        if (p.y_rows) return half ? launch<2, true, true, true>(p, smem, s) : launch<2, true, true, false>(p, smem, s);
+        return half ? launch<2, true, false, true>(p, smem, s) : launch<2, true, false, false>(p, smem, s);
+      }
+      return launch<2, false, true, true>(p, smem, s);
+    case 4: return launch<4, false, true, true>(p, smem, s);
+    default: return launch<8, false, true, true>(p, smem, s);
   }
 }

@@ -393,8 +393,8 @@ class LinearPlan:
         if out.dtype not in (torch.bfloat16, torch.float32):
             raise ValueError("output must be bf16 or f32")
         segs = [(int(b), int(e), int(s)) for b, e, s in segments]
-        if any(b % 16 for b, _, _ in segs):
-            raise ValueError("LinearPlan segments must start on 16-row boundaries (see align_segments)")
+        if any(b % 8 for b, _, _ in segs):
+            raise ValueError("LinearPlan segments must start on 8-row boundaries (see align_segments)")
         if len(segs) > _lib.MAX_SEGMENTS:
             raise NotImplementedError(f"more than {_lib.MAX_SEGMENTS} expert segments in one launch")
         self.geom = geom
@@ -601,23 +601,74 @@ def tune_num_ctas(key, make_plan, candidates, reps: int = 16, stream=None) -> in
     return best
 
 
+TMEM_ROW_BUDGET = 384  # base + delta accumulator columns per launch (512 TMEM columns - 2 A slots)
+
+
+def segment_align(n_rows: int) -> int:
+    """Row alignment of an expert group in a fused launch: groups of <= 8 rows take one
+    8-row half of a 16-row tcgen05 window (two such experts share a window: the kernel's
+    delta MMA for each covers the window and its epilogue reads only its own half), larger
+    groups start on a window."""
+    return 8 if n_rows <= 8 else 16
+
+
+def delta_columns(begin: int, end: int) -> int:
+    """Delta accumulator columns a segment takes: 16 per window it touches."""
+    return 16 * (((end - 1) >> 4) - (begin >> 4) + 1)
+
+
 def align_segments(B: int, segments) -> tuple:
-    """Re-layout rows so every expert segment starts at a multiple of 16 rows (the
-    kernel's tcgen05 N granularity).  Returns (rows_pad, new_segments, src) where
-    src[new_row] = old row or -1 for padding rows."""
+    """Re-layout rows so every expert segment starts on its alignment (segment_align: an
+    8-row half window for <= 8 rows, else a 16-row window -- the kernel's tcgen05 N
+    granularity).  Returns (rows_pad, new_segments, src) where src[new_row] = old row or
+    -1 for padding rows."""
     segs = sorted((int(b), int(e), int(s)) for b, e, s in segments)
     src, new_segs = [], []
     cur = 0
     for b, e, sl in segs:
         if cur < b:  # uncovered (base-only) rows keep their place in order
             src.extend(range(cur, b))
-        while len(src) % 16:
+        while len(src) % segment_align(e - b):
             src.append(-1)
         new_segs.append((len(src), len(src) + (e - b), sl))
         src.extend(range(b, e))
         cur = e
     src.extend(range(cur, B))
     return len(src), new_segs, src
+
+
+def launch_groups(B: int, segs: list, max_rows: int = None, tmem_cols: int = TMEM_ROW_BUDGET) -> list:
+    """Split rows [0, B) into fused launches: each <= max_rows padded rows (MAX_ROWS) with
+    base + delta accumulator columns (canonical_rows + sum of delta_columns) <= tmem_cols,
+    cut at 16-row boundaries, preferring segment starts; an oversized expert group is cut
+    too.  Returns [(r0, r1, segments rebased to r0)]."""
+    max_rows = MAX_ROWS if max_rows is None else max_rows
+    segs = sorted(segs)
+
+    def fits(r0, r1):
+        gs = [(max(b, r0) - r0, min(e, r1) - r0) for b, e, _ in segs if b < r1 and e > r0]
+        return (r1 - r0 <= max_rows and
+                canonical_rows(r1 - r0) + sum(delta_columns(b, e) for b, e in gs) <= tmem_cols)
+
+    cuts = [0]
+    while cuts[-1] < B:
+        r0 = cuts[-1]
+        bounds = {x for b, e, _ in segs for x in (b, e) if x > r0 and x % 16 == 0} | {B}
+        cands = sorted(bounds | set(range(r0 + 16, min(B, r0 + max_rows) + 1, 16)))
+        ok = []
+        for x in cands:
+            if not fits(r0, x):
+                break
+            ok.append(x)
+        if not ok:
+            raise NotImplementedError("a 16-row window does not fit one fused launch")
+        at_bound = [x for x in ok if x in bounds]  # prefer not to split an expert group
+        cuts.append(at_bound[-1] if at_bound else ok[-1])
+    groups = []
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        gs = [(max(b, r0) - r0, min(e, r1) - r0, sl) for b, e, sl in segs if b < r1 and e > r0]
+        groups.append((r0, r1, gs))
+    return groups
 
 
 _ME_PLANS: dict = {}
@@ -634,11 +685,8 @@ class _MeLinearPlan:
         dev = x.device
         rows, new_segs, src = align_segments(B, segs)
         self.launches = []
-        start = 0
-        while start < rows:
-            end = min(rows, start + MAX_ROWS)
+        for start, end, csegs in launch_groups(rows, new_segs):
             n_rows = end - start
-            csegs = [(max(b, start) - start, min(e, end) - start, sl) for b, e, sl in new_segs if b < end and e > start]
             src_t = torch.as_tensor(src[start:end], dtype=torch.int32, device=dev)
             xc = torch.empty(canonical_numel(n_rows, geom.m), dtype=torch.bfloat16, device=dev)
             corr = corr_table(n_rows, geom.m, dev) if (offset_codes and csegs) else None
@@ -648,7 +696,6 @@ class _MeLinearPlan:
                                   num_ctas, activation, x_corr=corr)
                 plan.args.y_rows = src_t.data_ptr()  # grouped launch row -> caller's row (or -1)
             self.launches.append((src_t, n_rows, xc, corr, plan))
-            start = end
         self.keep = (weight, table)  # identity-checked by me_linear (ids alone could be reused)
 
     def __call__(self, x, out, residual, stream=None):

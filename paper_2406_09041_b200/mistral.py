@@ -43,24 +43,9 @@ class LayerWeights:
 
 
 def _launch_groups(B: int, segs: list) -> list:
-    """Split engine rows [0, B) into launch groups of <= MAX_ROWS rows at 16-row boundaries
-    (segment boundaries preferred; an oversized expert group is cut too).  Returns
-    [(r0, r1, segments rebased to r0)]."""
-    from .device import MAX_ROWS
-    cuts = [0]
-    bounds = sorted({b for b, _, _ in segs} | {B})
-    for b in bounds:
-        while b - cuts[-1] > MAX_ROWS:
-            # last segment start inside the window, else a 16-row cut
-            inside = [x for x in bounds if cuts[-1] < x <= cuts[-1] + MAX_ROWS and x % 16 == 0 and x < b]
-            cuts.append(inside[-1] if inside else cuts[-1] + MAX_ROWS)
-    if cuts[-1] != B:
-        cuts.append(B)
-    groups = []
-    for r0, r1 in zip(cuts[:-1], cuts[1:]):
-        gs = [(max(b, r0) - r0, min(e, r1) - r0, sl) for b, e, sl in segs if b < r1 and e > r0]
-        groups.append((r0, r1, gs))
-    return groups
+    """Launch groups of the engine rows (device.launch_groups: row and TMEM budgets)."""
+    from .device import launch_groups
+    return launch_groups(B, segs)
 
 
 class CacheWindowError(ValueError):
@@ -279,9 +264,9 @@ class MistralMultiExpert:
 
     # ------------------------------------------------------------------ batch
     def set_batch(self, expert_ids: list, prompt_lens: list | None = None) -> np.ndarray:
-        """Fix the request batch.  Requests are regrouped by expert and every expert group
-        starts on a 16-row boundary (the fused kernel's tcgen05 N granularity); padding
-        rows are inert.  Returns `rows`: rows[r] = caller's request index at engine row r
+        """Fix the request batch.  Requests are regrouped by expert; every expert group starts
+        on a 16-row tcgen05 window, or on an 8-row half window when it holds <= 8 requests
+        (device.segment_align: two small experts share a window); padding rows are inert.  Returns `rows`: rows[r] = caller's request index at engine row r
         (-1 for padding).  Positions start at prompt_lens (cache rows below are assumed
         filled)."""
         n = len(expert_ids)
@@ -314,10 +299,11 @@ class MistralMultiExpert:
                 slots.append(self.experts[e][0])
         slots = np.asarray(slots)
         rows, segs = [], []
+        from .device import segment_align
         for sl in sorted(set(slots.tolist()) - {-1}):
-            while len(rows) % 16:
-                rows.append(-1)
             members = np.flatnonzero(slots == sl).tolist()
+            while len(rows) % segment_align(len(members)):  # <= 8 requests: half a 16-row window
+                rows.append(-1)
             segs.append((len(rows), len(rows) + len(members), int(sl)))
             rows.extend(members)
         rows.extend(np.flatnonzero(slots == -1).tolist())  # base-only requests

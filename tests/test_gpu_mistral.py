@@ -39,7 +39,7 @@ def _build(shape, n_experts=3, seed=0, B=5):
         lw["attn_norm"] = _bf(1 + 0.1 * rng.normal(size=s.hidden))
         lw["mlp_norm"] = _bf(1 + 0.1 * rng.normal(size=s.hidden))
         W["layers"].append(lw)
-    eng = MistralMultiExpert(s, max_batch=256, ctx_max=32)
+    eng = MistralMultiExpert(s, max_batch=512, ctx_max=32)
     eng.load_base(torch.from_numpy(W["embedding"]), torch.from_numpy(W["final_norm"]),
                   torch.from_numpy(W["head"]),
                   [{k: torch.from_numpy(v) for k, v in lw.items()} for lw in W["layers"]])
@@ -62,8 +62,10 @@ def _build(shape, n_experts=3, seed=0, B=5):
 
 @pytest.mark.parametrize("n_exp,experts", [
     (3, ["e1", "e0", "e2", "e1", None]),
-    # 13 expert windows of 16 rows = 208 rows > one launch: two launch groups per linear
+    # 13 experts of 1-2 requests: 8-row half windows (two experts per 16-row window)
     (13, [f"e{i}" for i in range(13)] + ["e3", None]),
+    # 13 experts of 9-10 requests: whole windows, 2 launch groups per linear (row / TMEM budget)
+    (13, [f"e{i % 13}" for i in range(13 * 9 + 5)] + [None]),
 ])
 def test_decode_step_matches_oracle(n_exp, experts):
     import torch
@@ -71,13 +73,13 @@ def test_decode_step_matches_oracle(n_exp, experts):
     eng, W, dense = _build(shape, n_experts=n_exp)
     B, prompt = len(experts), 6
     rows = eng.set_batch(experts, [prompt] * B)
-    if n_exp > 12:
-        assert len(eng.groups) == 2
+    if len(experts) > 100:
+        assert len(eng.groups) >= 2
     R = eng.B
     real = np.flatnonzero(rows >= 0)  # engine rows holding requests
     assert sorted(rows[real].tolist()) == list(range(B))
-    for b, e, sl in eng.segments:  # expert groups start on 16-row boundaries
-        assert b % 16 == 0
+    for b, e, sl in eng.segments:  # expert groups: <= 8 requests on a half window, else a window
+        assert b % (8 if e - b <= 8 else 16) == 0
     rng = np.random.default_rng(3)
     kc = _bf(rng.normal(0, 0.5, size=eng.kcache.shape))
     vc = _bf(rng.normal(0, 0.5, size=eng.vcache.shape))
