@@ -303,7 +303,9 @@ class ExpertTable:
 # --------------------------------------------------------------------------- workspace
 
 class Workspace:
-    """Split-K partials + self-resetting column-group counters for one stream."""
+    """Split-K partials + self-resetting column-group counters.  Launches that may run
+    concurrently must not share one: `get(device, stream)` keys it by stream (launches on one
+    stream are serialised, so they can)."""
 
     _per_device: dict = {}
 
@@ -318,11 +320,12 @@ class Workspace:
         self.counters = torch.zeros(1 << 14, dtype=torch.int32, device=self.device)
 
     @classmethod
-    def get(cls, device) -> "Workspace":
+    def get(cls, device, stream=None) -> "Workspace":
         device = torch.device(device)
-        key = device.index if device.index is not None else torch.cuda.current_device()
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        key = (idx, None if stream is None else int(stream.cuda_stream))
         if key not in cls._per_device:
-            cls._per_device[key] = cls(torch.device("cuda", key))
+            cls._per_device[key] = cls(torch.device("cuda", idx))
         return cls._per_device[key]
 
 
@@ -379,7 +382,7 @@ class LinearPlan:
     def __init__(self, xc: torch.Tensor, B: int, weight: DeviceWeight | None, table: ExpertTable | None,
                  segments, out: torch.Tensor, residual: torch.Tensor | None = None,
                  geom: LinearGeometry | None = None, num_ctas: int = 0, activation: str | None = None,
-                 x_corr: torch.Tensor | None = None):
+                 x_corr: torch.Tensor | None = None, stream=None):
         L = _lib.lib()
         if geom is None:
             geom = weight.geom if weight is not None else next(
@@ -399,7 +402,9 @@ class LinearPlan:
             raise NotImplementedError(f"more than {_lib.MAX_SEGMENTS} expert segments in one launch")
         self.geom = geom
         self.keep = (xc, weight, table, out, residual, x_corr)  # keep buffers alive
-        ws = Workspace.get(xc.device)
+        # the stream this plan is launched on (None: the default / engine stream); plans that
+        # run concurrently on different streams get different split-K workspaces
+        ws = Workspace.get(xc.device, stream)
         self.ws = ws
         a = _lib.LinearArgs()
         a.x = xc.data_ptr()
@@ -680,7 +685,7 @@ class _MeLinearPlan:
     and bias-table buffers and the bound launch plan(s) -- per call only the gather-pack and
     the fused launch run (two kernels, no host-side tensor ops)."""
 
-    def __init__(self, x, weight, table, segs, out, residual, geom, num_ctas, activation, offset_codes):
+    def __init__(self, x, weight, table, segs, out, residual, geom, num_ctas, activation, offset_codes, stream=None):
         B = x.shape[0]
         dev = x.device
         rows, new_segs, src = align_segments(B, segs)
@@ -693,7 +698,7 @@ class _MeLinearPlan:
             plan = None
             if weight is not None or csegs:
                 plan = LinearPlan(xc, n_rows, weight, table if csegs else None, csegs, out, residual, geom,
-                                  num_ctas, activation, x_corr=corr)
+                                  num_ctas, activation, x_corr=corr, stream=stream)
                 plan.args.y_rows = src_t.data_ptr()  # grouped launch row -> caller's row (or -1)
             self.launches.append((src_t, n_rows, xc, corr, plan))
         self.keep = (weight, table)  # identity-checked by me_linear (ids alone could be reused)
@@ -747,14 +752,18 @@ def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable |
         raise ValueError("out must be a row-contiguous bf16/f32 tensor with >= B rows")
     if residual is not None and (residual.dtype != torch.bfloat16 or residual.stride(1) != 1):
         raise ValueError("residual must be a row-contiguous bf16 tensor")
+    # per stream: concurrent calls on two streams must not share the cached canonical buffers
+    # or the split-K workspace
     key = (x.device, tuple(x.shape), x.stride(0), id(weight), id(table), segs, out.dtype, out.stride(0),
            residual.stride(0) if residual is not None else None, geom, num_ctas, activation, bool(offset_codes),
-           table.dev.data_ptr() if table is not None else None)
+           table.dev.data_ptr() if table is not None else None,
+           None if stream is None else int(stream.cuda_stream))
     plan = _ME_PLANS.get(key)
     if plan is None or plan.keep[0] is not weight or plan.keep[1] is not table:
         if len(_ME_PLANS) >= _ME_PLANS_MAX:
             _ME_PLANS.pop(next(iter(_ME_PLANS)))
-        plan = _MeLinearPlan(x, weight, table, segs, out, residual, geom, num_ctas, activation, offset_codes)
+        plan = _MeLinearPlan(x, weight, table, segs, out, residual, geom, num_ctas, activation, offset_codes,
+                             stream)
         _ME_PLANS[key] = plan
     plan(x, out, residual, stream)
     return out

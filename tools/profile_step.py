@@ -17,7 +17,9 @@ ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--experts", type=int, default=3)
 ap.add_argument("--layers", type=int, default=None)
 a = ap.parse_args()
-eng = bm.build_engine(a.batch, a.experts, n_layers=a.layers)
+E = a.experts
+eng = bm.build_engine(a.batch, list(range(E)), [i % E for i in range(a.batch)],  # balanced, as the router's
+                      max_batch=a.batch + 16 * E, n_layers=a.layers)
 eng.step()
 eng.step()
 torch.cuda.synchronize()
