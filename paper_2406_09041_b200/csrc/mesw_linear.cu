@@ -656,6 +656,8 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     constexpr int WPK = CHB / 4;  // code words per k-half of a channel
     const int n_dq = p.n_dq;
+    const int dq_mask = n_dq - 1, dq_shift = n_dq - 1;  // n_dq in {1, 2} (kDqGroups == 2)
+    static_assert(kDqGroups <= 2, "dequant bookkeeping assumes at most two groups");
     MESW_PROF(long long dprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};)
     MESW_PROF(const long long dstart = clock64();)
     MESW_PROF(int dcount = 0;)
@@ -682,8 +684,9 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
             // job is expanded and stored to TMEM, then ONE tcgen05.wait::st + fence covers the
             // batch before its slots are published -- the store-completion wait and the arrive
             // round trip were ~1/3 of a job's cycles when paid per job.
-            const int q_first = sg0 + ((grp - sg0 % n_dq) + n_dq) % n_dq;
-            const int n_jobs = (q_first < sg1 ? (sg1 - 1 - q_first) / n_dq + 1 : 0) * kJobHalves;
+            // n_dq is 1 or 2: mask / shift, no integer division in the per-chunk bookkeeping
+            const int q_first = sg0 + ((grp - (sg0 & dq_mask)) & dq_mask);
+            const int n_jobs = (q_first < sg1 ? ((sg1 - 1 - q_first) >> dq_shift) + 1 : 0) * kJobHalves;
             for (int j0 = 0, nb = 0; j0 < n_jobs; j0 += nb) {
               nb = min(min(kDqBatch, n_jobs - j0), na);  // distinct slots only
               int slots[kDqBatch];

@@ -11,8 +11,17 @@ L.mesw_debug_timing_copy.argtypes = [C.c_void_p, C.c_int]
 m, n = int(sys.argv[1]), int(sys.argv[2])
 E, rows = int(sys.argv[3]), int(sys.argv[4])
 sets = [make(m, n, max(E, 1), r) for r in range(3)]  # rotate replicas: the timed launch is HBM-cold
-segs = [(16 * i, 16 * i + 3, i) for i in range(E)] if E else []
-rows = max(rows, 16 * (E - 1) + 3) if E else rows
+if os.environ.get("ALIGNED"):  # B = rows tokens split evenly over E experts, serving-engine alignment
+    from paper_2406_09041_b200.device import align_segments
+    per = [rows // E + (1 if i < rows % E else 0) for i in range(E)]
+    segs, cur = [], 0
+    for e, c_ in enumerate(per):
+        segs.append((cur, cur + c_, e))
+        cur += c_
+    rows, segs, _ = align_segments(rows, segs)
+else:
+    segs = [(16 * i, 16 * i + 3, i) for i in range(E)] if E else []
+    rows = max(rows, 16 * (E - 1) + 3) if E else rows
 x = torch.randn((rows, m), device="cuda").to(torch.bfloat16)
 y = torch.empty((rows, n), dtype=torch.bfloat16, device="cuda")
 corr = corr_table(rows, m, "cuda") if os.environ.get("EXACT") is None else None
