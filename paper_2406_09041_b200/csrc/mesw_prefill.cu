@@ -18,14 +18,15 @@
 //
 // Work: tiles (column-group pair, 256-token tile = two 128-token expert groups), persistent
 // CTA pairs walk tiles cg-pair-major so the pairs running at the same time share W tiles in L2.
-// Roles per CTA (16 warps):
+// Roles per CTA (24 warps at the default MESW_PF_GROUPS = 4):
 //   warps 0, 2  producers (one thread each): W unit (32 KiB) + the two groups' code units
 //               (4 KiB each); this CTA's half of the x tile (32 KiB: 2 groups x 8 windows x 2 KiB).
 //   warp 1      leader: MMA issuer (M = 256 over the pair, N = 128 per group, K = 16);
 //               peer: relays "x half landed" to the leader's barrier.
-//   warps 4-11  two merge groups: group g owns k-half g of every unit, thread = output row;
-//               LDS of W + codes, bf16x2 fma merge, tcgen05.st into the A slot of each group.
-//   warps 12-15 epilogue: tcgen05.ld of the 2 x 128-column accumulators, y stores.
+//   warps 4-19  four merge groups: group g owns k-slice g (32 inputs) of every unit, thread =
+//               output row; LDS of W + codes, bf16x2 fma merge, tcgen05.st into the A slot.
+//   warps 20-23 epilogue: tcgen05.ld of the 2 x 128-column accumulators, y stores; each
+//               128-token group's accumulator is released as soon as it is drained.
 // TMEM: accumulators [group 0 | group 1] x 128 columns, then 4 A slots of 64 columns.
 
 #include <stdlib.h>
