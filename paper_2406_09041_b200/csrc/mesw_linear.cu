@@ -36,6 +36,11 @@ namespace mesw {
 #ifndef MESW_DQ_GROUPS
 #define MESW_DQ_GROUPS 2
 #endif
+#ifdef MESW_PROFILE
+#define MESW_PROF(...) __VA_ARGS__
+#else
+#define MESW_PROF(...)
+#endif
 constexpr int kDqGroups = MESW_DQ_GROUPS;  // dequant warpgroups: group g fills the A slots s with s % kDqGroups == g
 // warp roles: 0 producer (codes, weight tiles, activations), 1-3 MMA issuers, 4-11 two dequant groups, 12-15 epilogue (TMEM lane quarters = warp % 4)
 constexpr int kProdWarp = 0, kMmaWarp = 1;
@@ -259,7 +264,8 @@ __device__ __forceinline__ int out_row(const LinearParams& p, const Smem& S, int
 struct EpiPre {
   int sg[2];
   float sj[2];
-  float R[kSalFast];  // salient rows of the first half's segment (the second half reloads if it differs)
+  float R[kSalFast];   // salient rows of the first half's segment (or the second's if the first is empty)
+  float R1[kSalFast];  // HALF: the second half's segment when it differs from the first
   float res[16];
 };
 
@@ -284,6 +290,11 @@ __device__ __forceinline__ void epi_prefetch(const LinearParams& p, const Smem& 
 #pragma unroll
   for (int r = 0; r < kSalFast; ++r) e.R[r] = 0.f;
   if (fast && sr >= 0 && j < p.n) load_sal_rows(S, sr, m, e.R);
+  if (HALF) {
+#pragma unroll
+    for (int r = 0; r < kSalFast; ++r) e.R1[r] = 0.f;
+    if (fast && s0 >= 0 && s1 >= 0 && s1 != s0 && j < p.n) load_sal_rows(S, s1, m, e.R1);
+  }
 #pragma unroll
   for (int t = 0; t < 16; ++t)
     e.res[t] = (p.residual && t0 + t < p.B && j < p.n && out_row<YMAP>(p, S, t0 + t) >= 0)
@@ -291,28 +302,40 @@ __device__ __forceinline__ void epi_prefetch(const LinearParams& p, const Smem& 
 }
 
 // Thread owns output channel j = cg*128 + m; accumulators for the 16 rows [t0, t0+16).
+// All 16 outputs are formed first and stored after: stores through the generic y pointer
+// may alias shared memory, so interleaving them with the rows' smem reads serialised the
+// rows (~300 cycles per row in the final stream-K reductions, measured).
 template <bool YMAP, bool HALF>
 __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S, int cg, int m, int t0,
-                                            const float* vb, const float* vd, bool fast, const EpiPre& e) {
+                                            const float* vb, const float* vd, bool fast, const EpiPre& e,
+                                            bool dry = false) {
   const int j = cg * kUnitN + m;
   if (j >= p.n) return;
-  float R[kSalFast];
+  const bool two = HALF && e.sg[0] >= 0 && e.sg[1] >= 0 && e.sg[1] != e.sg[0];  // second half: other rows
+  float out[16];
+  if (fast) {
+    // straight-line: no per-row branch, so the 16 rows' smem reads and fma chains overlap
+    // (a data-dependent branch per row serialised them: ~170 cycles per row, measured)
 #pragma unroll
-  for (int r = 0; r < kSalFast; ++r) R[r] = e.R[r];
-#pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const int tok = t0 + t;
-    if (tok >= p.B) break;
-    float v = vb[t];
-    const int h = HALF ? (t >> 3) : 0;
-    if (HALF && t == 8 && fast && e.sg[1] >= 0 && e.sg[0] >= 0 && e.sg[1] != e.sg[0])
-      load_sal_rows(S, e.sg[1], m, R);  // second half of the window: another expert's rows
-    if (e.sg[h] >= 0 && S.tok2seg[tok] == e.sg[h]) {
+    for (int t = 0; t < 16; ++t) {
+      const int tok = t0 + t;
+      const int h = HALF ? (t >> 3) : 0;
+      const bool match = tok < p.B && e.sg[h] >= 0 && S.tok2seg[tok] == e.sg[h];
       float d = e.sj[h] * vd[t];
-      if (fast) {
 #pragma unroll
-        for (int r = 0; r < kSalFast; ++r) d = fmaf(S.xsal[tok][r], R[r], d);
-      } else {
+      for (int r = 0; r < kSalFast; ++r) d = fmaf(S.xsal[tok][r], (h == 1 && two) ? e.R1[r] : e.R[r], d);
+      float v = vb[t] + (match ? d : 0.f) + e.res[t];
+      if (p.activation == 1) v = fmaxf(v, 0.f);
+      out[t] = v;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int tok = t0 + t;
+      float v = vb[t];
+      const int h = HALF ? (t >> 3) : 0;
+      if (tok < p.B && e.sg[h] >= 0 && S.tok2seg[tok] == e.sg[h]) {
+        float d = e.sj[h] * vd[t];
         const SegDesc& sd = S.segs[e.sg[h]];
         const int r0 = sd.sal_off[cg], k = sd.sal_off[cg + 1] - r0;
         for (int r = 0; r < k; ++r) {
@@ -320,17 +343,25 @@ __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S
           const float rv = __half2float(__ushort_as_half(sd.sal_rows[(size_t)(r0 + r) * kUnitN + m]));
           d = fmaf(xv, rv, d);
         }
+        v += d;
       }
-      v += d;
+      v += e.res[t];
+      if (p.activation == 1) v = fmaxf(v, 0.f);
+      out[t] = v;
     }
-    v += e.res[t];
-    if (p.activation == 1) v = fmaxf(v, 0.f);
+  }
+  MESW_PROF(if (p.tbuf && threadIdx.x == 0) p.tbuf[4096 * 12 + (size_t)blockIdx.x * 8 + 2] = clock64();)
+  if (dry) return;
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int tok = t0 + t;
+    if (tok >= p.B) break;
     const int orow = out_row<YMAP>(p, S, tok);
     if (orow < 0) continue;
     if (p.y_bf16)
-      reinterpret_cast<__nv_bfloat16*>(p.y)[(size_t)orow * p.ldy + j] = __float2bfloat16_rn(v);
+      reinterpret_cast<__nv_bfloat16*>(p.y)[(size_t)orow * p.ldy + j] = __float2bfloat16_rn(out[t]);
     else
-      reinterpret_cast<float*>(p.y)[(size_t)orow * p.ldy + j] = v;
+      reinterpret_cast<float*>(p.y)[(size_t)orow * p.ldy + j] = out[t];
   }
 }
 
@@ -342,7 +373,7 @@ __device__ __forceinline__ void epi_store16(const LinearParams& p, const Smem& S
 template <bool YMAP, bool HALF>
 __device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& S, int cg, int cgp, int rank, int m,
                                           int t0, int p_first, int p_last, bool fast, const EpiPre& pre,
-                                          const float* stage) {
+                                          const float* stage, bool dry = false) {
   const int NP = p.NP;
   const long long T2 = p.T, G2 = p.G / 2;
   const size_t slot_floats = (size_t)NP * kUnitN;
@@ -365,7 +396,8 @@ __device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& 
 #pragma unroll
     for (int i = 0; i < 16; ++i) vb[i] += lb[i];
   }
-  epi_store16<YMAP, HALF>(p, S, cg, m, t0, vb, vd, fast, pre);
+  MESW_PROF(if (p.tbuf && threadIdx.x == 0) p.tbuf[4096 * 12 + (size_t)blockIdx.x * 8 + 1] = clock64();)
+  epi_store16<YMAP, HALF>(p, S, cg, m, t0, vb, vd, fast, pre, dry);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -375,11 +407,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // Cycle-count profiling of the role loops (tools/ktiming.py): compiled in only with
 // -DMESW_PROFILE (MESW_PROFILE=1 python build.py --force); zero cost otherwise.
-#ifdef MESW_PROFILE
-#define MESW_PROF(...) __VA_ARGS__
-#else
-#define MESW_PROF(...)
-#endif
 #define MESW_STAMP(i) \
   do { if (p.tbuf) p.tbuf[(size_t)blockIdx.x * 8 + (i)] = gtimer(); } while (0)
 // second stamp bank (tail phases, SM clock cycles: %globaltimer reads of different warps of
@@ -936,13 +963,22 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     }
     MESW_PROF(fp[1] += clock64() - fq; fq = clock64();)
     if (threadIdx.x == 0) MESW_STAMP2(4);
+#ifdef MESW_EXP_WARM
+    for (int pass = 0; pass < 2; ++pass) {  // diagnostic: pass 0 runs the same code without stores
+      const bool dry = pass == 0;
+      if (pass == 1 && threadIdx.x == 0) MESW_STAMP2(7);
+#else
+    {
+      const bool dry = false;
+#endif
     for (int t0 = t_first; t0 < NP; t0 += 16 * (kThreads / kUnitN)) {
       EpiPre pre;
       if (t0 == t_first) pre = pre0;
       else epi_prefetch<YMAP, HALF>(p, S, fcg, fm, t0, ffast, pre);
-      if (staged) reduce_chunk<YMAP, HALF>(p, S, fcg, fcgp, (int)rank, fm, t0, pf, nC <= nbuf ? pl : pf, ffast, pre, st);
-      else reduce_chunk<YMAP, HALF>(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre, nullptr);
+      if (staged) reduce_chunk<YMAP, HALF>(p, S, fcg, fcgp, (int)rank, fm, t0, pf, nC <= nbuf ? pl : pf, ffast, pre, st, dry);
+      else reduce_chunk<YMAP, HALF>(p, S, fcg, fcgp, (int)rank, fm, t0, pf, pl, ffast, pre, nullptr, dry);
       MESW_PROF(fp[2] += clock64() - fq; fq = clock64();)
+    }
     }
     MESW_PROF(fp[3] = staged ? nC : -nC;)
     MESW_PROF(if (p.tbuf && threadIdx.x == 0) for (int i = 0; i < 4; ++i) p.tbuf[4096 * 40 + (size_t)blockIdx.x * 16 + i] = fp[i];)

@@ -62,7 +62,8 @@ flag = t2[:, 7]
 print("    epilogue done when thread 0 passed the final barrier:", int((flag == 1001).sum()), "of", int((flag >= 1000).sum()))
 print("  tail (bank 2: SM clock cycles, per CTA):")
 for nm, a_, b_ in [("atomic", 0, 1), ("atomic->synced(epi)", 1, 2), ("synced->copies_landed", 2, 3),
-                   ("copies->summed", 3, 4), ("summed->reduced", 4, 5), ("cluster_sync", 5, 6)]:
+                   ("copies->summed", 3, 4), ("summed->reduced", 4, 5), ("cluster_sync", 5, 6),
+                   ("summed->pass1 (MESW_EXP_WARM)", 4, 7), ("pass1->reduced", 7, 5)]:
     ok = (t2[:, a_] > 0) & (t2[:, b_] > 0)
     if ok.any():
         d = (t2[ok, b_] - t2[ok, a_])
@@ -101,3 +102,9 @@ if t0c:
         if v.size:
             print(f"  deq{g} jobs (start, +slot, +stored, +arrived):",
                   " ".join(f"{a - t0c}/{b - a}/{c - b}/{d - c}" for a, b, c, d in v[:14]))
+fs = buf[4096 * 12:4096 * 12 + G * 8].reshape(G, 8).astype(np.int64)
+t4 = t2[:, 4]
+ok = (t4 > 0) & (fs[:, 1] > 0) & (fs[:, 2] > 0)
+if ok.any():
+    print("  final reduce, thread 0 (cycles): summed->chunk_sum", int(np.median(fs[ok, 1] - t4[ok])),
+          " chunk_sum->outputs", int(np.median(fs[ok, 2] - fs[ok, 1])), " outputs->reduced", int(np.median(t2[ok, 5] - fs[ok, 2])))
