@@ -64,6 +64,9 @@ constexpr int kAColsPerSlot = 64 / kJobHalves;
 constexpr int kMaxRows = 192;  // padded token rows per launch (TMEM: 2 * rows <= 384)
 constexpr int kMaxStages = 8;
 constexpr int kMaxCStages = 16;
+#ifndef MESW_STAGE_MIN
+#define MESW_STAGE_MIN 0
+#endif
 constexpr int kSalFast = 8;            // salient rows per column group handled from smem
 
 struct SegDesc {
@@ -925,7 +928,10 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     const size_t slot_floats = (size_t)NP * kUnitN, slot_bytes = slot_floats * sizeof(float);
     const int nC = pl - pf + 1;
     const int nbuf = (int)((size_t)p.ring_bytes / slot_bytes);
-    const bool staged = nbuf >= 2 || nC == 1;
+    // few contributors: every thread loads its 16 x nC partial values straight from L2 (one
+    // round trip); many (small linears split a column group over many pairs): bulk-copy
+    // batches into the idle smem ring
+    const bool staged = nC > MESW_STAGE_MIN && (nbuf >= 2 || nC == 1);
     float* st = reinterpret_cast<float*>(ring);
     const int t_first = 16 * (threadIdx.x / kUnitN);
     EpiPre pre0;
