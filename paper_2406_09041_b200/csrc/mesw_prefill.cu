@@ -54,7 +54,14 @@ constexpr int kGroupTok = 128;
 constexpr int kASlots = 4;
 constexpr int kACols = 64;
 constexpr int kAccCols = 2 * kGroupTok;
-constexpr int kNW = 2, kNX = 4, kNC = 4;  // ring depths (W / x / codes): x is held until the MMAs finish
+#ifndef MESW_PF_NW
+#define MESW_PF_NW 2
+#endif
+#ifndef MESW_PF_NX
+#define MESW_PF_NX 4
+#endif
+// ring depths (W / x / codes): x is held until the MMAs finish; (3, 3) measured equal to (2, 4)
+constexpr int kNW = MESW_PF_NW, kNX = MESW_PF_NX, kNC = 4;
 constexpr int kXBytes = kTileTok / 2 * kUnitK * 2;  // this CTA's half of the x tile: 32 KiB
 constexpr int kCBytes = 2 * 4096;                   // two groups' 2-bit code units
 constexpr int kSmemBytes = 232448;
