@@ -227,11 +227,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
   const uint16_t* kb = kc + (((size_t)b * ctx_max + t0) * n_kv + g) * D;
   const uint16_t* vb = vc + (((size_t)b * ctx_max + t0) * n_kv + g) * D;
   const int n_cached = ROPE && t0 + n == L ? n - 1 : n;  // ROPE: the last row is the new token
+  // cp.async: every thread's 16-byte K / V copies are in flight together (one wait below)
   for (int i = tid; i < n_cached * 16; i += kAttnThreads) {
     const int t = i >> 4, c = i & 15;
-    *reinterpret_cast<uint4*>(Ks + t * kAttnRow + c * 8) = __ldg(reinterpret_cast<const uint4*>(kb + t * kv_stride + c * 8));
-    *reinterpret_cast<uint4*>(Vs + t * kAttnRow + c * 8) = __ldg(reinterpret_cast<const uint4*>(vb + t * kv_stride + c * 8));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(Ks + t * kAttnRow + c * 8)),
+                 "l"(kb + t * kv_stride + c * 8) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(Vs + t * kAttnRow + c * 8)),
+                 "l"(vb + t * kv_stride + c * 8) : "memory");
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   const uint16_t* qrow = q + (size_t)b * ld_q;
   if (ROPE) {
     const int p = L - 1;
@@ -276,6 +280,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
     for (int i = tid; i < G * D; i += kAttnThreads)
       qs[i] = bf16_to_f32(qrow[(size_t)g * G * D + i]) * scale;
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // scores: thread -> (head h, positions t, t + 32 ...) with 128 / G threads per head
   constexpr int TPH = kAttnThreads / G;
