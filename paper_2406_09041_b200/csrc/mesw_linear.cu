@@ -282,7 +282,7 @@ __device__ __forceinline__ void load_sal_rows(const Smem& S, int sg, int m, floa
 
 template <bool YMAP, bool HALF>
 __device__ __forceinline__ void epi_prefetch(const LinearParams& p, const Smem& S, int cg, int m, int t0,
-                                             bool fast, EpiPre& e) {
+                                             bool fast, EpiPre& e, bool full = true) {
   const int j = cg * kUnitN + m;
   const int s0 = S.half2seg[t0 >> 3], s1 = HALF ? S.half2seg[(t0 >> 3) + 1] : s0;
   e.sg[0] = s0;
@@ -292,6 +292,7 @@ __device__ __forceinline__ void epi_prefetch(const LinearParams& p, const Smem& 
   const int sr = e.sg[0] >= 0 ? e.sg[0] : e.sg[1];
 #pragma unroll
   for (int r = 0; r < kSalFast; ++r) e.R[r] = 0.f;
+  if (!full) return;  // stream-K partial pieces use only sg / sj (the final reducer reloads the rest)
   if (fast && sr >= 0 && j < p.n) load_sal_rows(S, sr, m, e.R);
   if (HALF) {
 #pragma unroll
@@ -801,7 +802,11 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       const int cgp = po.cg_of(pi);
       const int cg = 2 * cgp + (int)rank;
       const long long cg_end = (long long)(cgp + 1) * p.n_ks;
+#ifdef MESW_EXP_NORED
+      const bool whole = true;  // experiment: no stream-K reduction (wrong sums; bounds the tail cost)
+#else
       const bool whole = (u == (long long)cgp * p.n_ks) && (piece_end == cg_end);
+#endif
       const bool fast = gather_salient_x(p, S, cg, gtid);
       if (OFF) {  // offset-code bias of each token over this piece's k-steps (table: 4 B / token / k-step)
         const int ks0 = (int)(u - (long long)cgp * p.n_ks), ks1 = (int)(piece_end - (long long)cgp * p.n_ks);
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
         named_bar_sync(1, 128);
       }
       EpiPre pre;
-      epi_prefetch<YMAP, HALF>(p, S, cg, mrow, 0, fast, pre);
+      epi_prefetch<YMAP, HALF>(p, S, cg, mrow, 0, fast, pre, whole);
       mbar_wait_sleep(&S.accfull[ab], (uint32_t)(acc_use[ab] & 1));
       tc_fence_after();
       if (gtid == 0 && pi == po.np - 1) MESW_STAMP(5);
@@ -862,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) __stcg(mine + (size_t)(t0 + i) * kUnitN + mrow, vb[i]);
-          if (t0 + 16 < NP) epi_prefetch<YMAP, HALF>(p, S, cg, mrow, t0 + 16, fast, pre);
+          if (t0 + 16 < NP) epi_prefetch<YMAP, HALF>(p, S, cg, mrow, t0 + 16, fast, pre, false);
         }
       }
       // accumulators consumed -> the leader may reuse this buffer

@@ -27,11 +27,12 @@ y = torch.empty((rows, n), dtype=torch.bfloat16, device="cuda")
 corr = corr_table(rows, m, "cuda") if os.environ.get("EXACT") is None else None
 xc = pack_x(x, corr=corr)
 nobase = os.environ.get("NOBASE") is not None  # delta-only launches (no base weight)
-plans = [LinearPlan(xc, rows, None if nobase else dw, table if E else None, segs, y, geom=geom, x_corr=corr) for geom, dw, table in sets]
+CT = int(os.environ.get("CTAS", "0"))
+plans = [LinearPlan(xc, rows, None if nobase else dw, table if E else None, segs, y, geom=geom, x_corr=corr, num_ctas=CT) for geom, dw, table in sets]
 for i in range(6): plans[i % 3]()
 torch.cuda.synchronize()
 plans[0](); torch.cuda.synchronize()
-G = min(148, (n // 128) * (m // 128))
+G = min(CT or 148, (n // 128) * (m // 128))
 G -= G % 2
 buf = np.zeros(60 * 4096, np.uint64)
 _lib.check(L.mesw_debug_timing_copy(buf.ctypes.data, G))
