@@ -17,12 +17,16 @@
  *    y = x . W.
  *
  * Device layouts: a linear with m inputs
- * and n outputs is padded to m_pad = ceil(m/128)*128, n_pad = ceil(n/128)*128
- * and cut into column groups (cg, 128 outputs) x k-steps (ks, 128 inputs).
- *  - base weight  : bf16, [cg][ks][tile 8][kblock 8][lane 32][8 elems]
- *                   (one mma.m16n8k16 A fragment per lane per k-block; 32 KiB per (cg,ks))
+ * and n outputs is padded to m_pad = ceil(m/128)*128, n_pad = ceil(n/256)*256
+ * (column groups come in pairs: one tcgen05 cta_group::2 MMA covers two) and cut
+ * into column groups (cg, 128 outputs) x k-steps (ks, 128 inputs), stored cg-major.
+ *  - base weight  : bf16, one 32 KiB unit per (cg, ks) in the UMMA K-major
+ *                   SWIZZLE_NONE canonical layout (8 x 16 B core matrices, LBO 128 B,
+ *                   SBO 2048 B): one bulk copy lands a ready tcgen05 A operand
  *  - delta codes  : DB-bit device codes d = q + OFF (DB=2: b=2, OFF=2; DB=4:
- *                   b in {1,3,4}, OFF=8; DB=8: b=8, OFF=128), [cg][ks][tile][lane][8*DB bytes];
+ *                   b in {1,3,4}, OFF=8; DB=8: b=8, OFF=128), same unit order,
+ *                   2048*DB bytes per unit: per (k-half, output channel) 8*DB
+ *                   contiguous bytes in bf16x2-pair order;
  *                   salient input rows forced to d = OFF (q = 0), which keeps the fused
  *                   result equal to CompressedDelta.reconstruct() (compress.py:115-121)
  *  - steps        : f32 [n_pad]
@@ -106,7 +110,7 @@ int mesw_repack_codes(const uint8_t* d_packed, uint32_t m, uint32_t n, uint32_t 
                       uint32_t m_pad, uint32_t n_total_pad, uint32_t col_base,
                       void* stream);
 
-/* Repack a bf16 base weight into the fragment layout.  If `transposed` == 0 the
+/* Repack a bf16 base weight into the canonical tile layout.  If `transposed` == 0 the
  * source is [m][ld] (reference orientation, rows = inputs); otherwise [n][ld]
  * (torch nn.Linear weight, rows = outputs).  Written at column offset col_base. */
 int mesw_repack_weight(const uint16_t* d_src, uint32_t m, uint32_t n, uint32_t ld,
@@ -136,7 +140,7 @@ int mesw_dequant_debug(const uint8_t* d_codes, uint32_t code_bits, const float* 
                        const int32_t* d_sal_off, const int32_t* d_sal_idx,
                        const uint16_t* d_sal_rows, uint32_t m, uint32_t n, uint32_t m_pad,
                        uint32_t n_total_pad, uint32_t col_base, float* d_out, void* stream);
-/* Debug: fragment-layout base weight -> bf16 [m][n] (reference orientation). */
+/* Debug: canonical-layout base weight -> bf16 [m][n] (reference orientation). */
 int mesw_unpack_weight_debug(const uint16_t* d_w, uint32_t m, uint32_t n, uint32_t m_pad,
                              uint32_t n_total_pad, uint32_t col_base, uint16_t* d_out,
                              void* stream);
@@ -165,7 +169,7 @@ typedef struct {
   int32_t B, m, n;   /* n: output columns written; device buffers must cover
                          ceil(n/256)*256 columns (column groups come in pairs) */
   int32_t x_layout;   /* must be 0 (canonical)                                 */
-  const uint16_t* w;  /* fragment-layout bf16 base, or NULL (delta only)      */
+  const uint16_t* w;  /* canonical-layout bf16 base, or NULL (delta only)     */
   const mesw_expert_dev* expert_table; /* DEVICE array indexed by slot        */
   int32_t code_bits;  /* 2, 4 or 8: shared by all experts of the launch       */
   int32_t n_segments; /* <= MESW_MAX_SEGMENTS                                 */
