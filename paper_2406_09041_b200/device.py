@@ -717,6 +717,34 @@ class _MeLinearPlan:
             plan(stream)
 
 
+class MeLinearGraph:
+    """`me_linear` on fixed buffers captured once in a CUDA graph (the form a serving loop
+    uses for a repeated call shape): the device-side row gather, the bias table and the fused
+    launch replay as one graph launch.  Callers copy new inputs into `x` (and `residual`)
+    and read `out` after `__call__`, on the stream they replay on."""
+
+    def __init__(self, x: torch.Tensor, weight: "DeviceWeight | None", table: "ExpertTable | None", segments,
+                 out: torch.Tensor, residual: torch.Tensor | None = None, **kw):
+        self.x, self.out, self.residual = x, out, residual
+        dev = x.device
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):  # warm: plan, kernel attributes, launch-width tuning
+            me_linear(x, weight, table, segments, out=out, residual=residual, stream=s, **kw)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            me_linear(x, weight, table, segments, out=out, residual=residual, stream=s, **kw)
+            g.capture_end()
+        torch.cuda.current_stream(dev).wait_stream(s)
+        self.graph = g
+
+    def __call__(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.out
+
+
 def me_linear(x: torch.Tensor, weight: DeviceWeight | None, table: ExpertTable | None,
               segments, out: torch.Tensor | None = None, residual: torch.Tensor | None = None,
               out_dtype=torch.bfloat16, geom: LinearGeometry | None = None, num_ctas: int = 0,

@@ -293,3 +293,14 @@ def test_me_linear_caller_row_order_on_device():
     yg = me_linear(xg, dw, table, [(0, 5, 2), (16, 17, 0), (32, 43, 1)], residual=rg, out_dtype=torch.float32)
     want = torch.stack([yg[order.index(r)] for r in range(B)])
     assert torch.equal(y1, want) and torch.equal(y2, want)
+    # the same call captured once and replayed on new inputs (device.MeLinearGraph)
+    from paper_2406_09041_b200.device import MeLinearGraph
+    xs, ys = torch.zeros_like(x), torch.empty((B, n), dtype=torch.float32, device="cuda")
+    rs = torch.zeros_like(res)
+    g = MeLinearGraph(xs, dw, table, segs, ys, residual=rs)
+    xs.copy_(x)
+    rs.copy_(res)
+    assert torch.equal(g(), want)
+    x2 = torch.flip(x, [0]).contiguous()
+    xs.copy_(x2)
+    assert torch.equal(g(), me_linear(x2, dw, table, segs, residual=res, out_dtype=torch.float32))
