@@ -279,7 +279,12 @@ int mesw_attention_decode(const uint16_t* d_q, int ld_q, const uint16_t* d_kcach
  * token's [q heads | k heads | v heads] row (not yet rotated), at position len[b] - 1
  * (callers keep len = pos + 1).  Rotates q per split, rotates k and appends k / v to the
  * caches from the split holding the new position, then attends as mesw_attention_decode.
- * Same results, bit for bit, as the two-call form; one launch fewer per layer. */
+ * Same results, bit for bit, as the two-call form; one launch fewer per layer.
+ * Contract (the decode engine's): len[] and the cached rows [0, len[b] - 1) are read before
+ * the kernel's PDL wait (only the new token's qkv row after it), so they must be complete
+ * when the kernels between their writer and this launch start: written before a kernel
+ * that does not trigger its dependents early (mesw_advance_positions, any non-libmesw
+ * kernel, a memcpy) or before a graph launch. */
 int mesw_attention_decode_rope(const uint16_t* d_qkv, int ld_qkv, uint16_t* d_kcache,
                                uint16_t* d_vcache, const int32_t* d_len, int B, int n_heads,
                                int n_kv, int head_dim, float theta, int ctx_max, uint16_t* d_out,

@@ -212,7 +212,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
     const int32_t* __restrict__ len, int n_kv, int ctx_max, float scale, float* __restrict__ part, int S,
     float theta) {
   pdl_trigger();
-  pdl_wait();  // inputs may come from the previous kernel in the stream
+  // ROPE (the decode engine's fused form): len and the cached rows were written by earlier
+  // decode steps, only the new token's q / k / v row comes from the previous kernel -- the
+  // K / V stream starts before the wait, under the tail of the qkv linear
+  if (!ROPE) pdl_wait();  // inputs may come from the previous kernel in the stream
   constexpr int D = 128;
   __shared__ __align__(16) uint16_t Ks[kAttnSplit * kAttnRow];
   __shared__ __align__(16) uint16_t Vs[kAttnSplit * kAttnRow];
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
                  "l"(vb + t * kv_stride + c * 8) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+  if (ROPE) pdl_wait();  // the new token's fused qkv row
   const uint16_t* qrow = q + (size_t)b * ld_q;
   if (ROPE) {
     const int p = L - 1;
@@ -508,7 +512,9 @@ __global__ void unpack_x_kernel(const uint16_t* __restrict__ xc, int B, int m, i
 // wrap_to < 0 (serving): no wrap -- the host refuses a step that would pass the window.
 __global__ void advance_kernel(int32_t* __restrict__ pos, int32_t* __restrict__ len, int B, int ctx_max,
                                int wrap_to) {
-  pdl_trigger();
+  // no early trigger: the next step's kernels launch only after the positions are written,
+  // so the whole previous step (and len) is complete before any of them starts -- the fused
+  // decode attention reads len and the cached rows before its PDL wait
   pdl_wait();  // inputs may come from the previous kernel in the stream
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
