@@ -347,14 +347,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
 }
 
 // Merge the splits of one (request, head): out = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s.
+// PRE (the fused decode form): len is complete before the launch (see attn_partial_kernel),
+// so it is read before the PDL wait and only the partials after it.
+template <bool PRE>
 __global__ void __launch_bounds__(128) attn_merge_kernel(const float* __restrict__ part, const int32_t* __restrict__ len,
                                                          int n_heads, int S, uint16_t* __restrict__ out, int ld_out,
                                                          int out_np, float* __restrict__ corr, int corr_ld) {
   __shared__ float red[4];
   pdl_trigger();
-  pdl_wait();
+  if (!PRE) pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const int Sb = (len[b] + kAttnSplit - 1) / kAttnSplit;
+  if (PRE) pdl_wait();
   const float* pp = part + ((size_t)b * n_heads + h) * (size_t)S * kAttnPart;
   float M = -INFINITY;
   for (int s2 = 0; s2 < Sb; ++s2) M = fmaxf(M, pp[(size_t)s2 * kAttnPart]);
@@ -600,8 +604,10 @@ static int attention_decode(const uint16_t* d_q, int ld_q, uint16_t* d_kcache, u
   }
 #undef MESW_ATTN_CASE
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
-  e = mesw_launch(attn_merge_kernel, dim3(B, n_heads), dim3(128), 0, s, (const float*)part, d_len, n_heads, S, d_out,
-                  ld_out, out_np, d_corr, corr_ld);
+  e = rope ? mesw_launch(attn_merge_kernel<true>, dim3(B, n_heads), dim3(128), 0, s, (const float*)part, d_len, n_heads,
+                         S, d_out, ld_out, out_np, d_corr, corr_ld)
+           : mesw_launch(attn_merge_kernel<false>, dim3(B, n_heads), dim3(128), 0, s, (const float*)part, d_len,
+                         n_heads, S, d_out, ld_out, out_np, d_corr, corr_ld);
   if (e != cudaSuccess) return mesw_fail(MESW_ERR_CUDA, cudaGetErrorString(e));
   return mesw_check_launch("attention_decode");
 }
