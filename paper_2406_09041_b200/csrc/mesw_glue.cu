@@ -361,12 +361,33 @@ __global__ void __launch_bounds__(128) attn_merge_kernel(const float* __restrict
   if (PRE) pdl_wait();
   const float* pp = part + ((size_t)b * n_heads + h) * (size_t)S * kAttnPart;
   float M = -INFINITY;
-  for (int s2 = 0; s2 < Sb; ++s2) M = fmaxf(M, pp[(size_t)s2 * kAttnPart]);
   float num = 0.f, den = 0.f;
-  for (int s2 = 0; s2 < Sb; ++s2) {
-    const float w = __expf(pp[(size_t)s2 * kAttnPart] - M);
-    den = fmaf(w, pp[(size_t)s2 * kAttnPart + 1], den);
-    num = fmaf(w, pp[(size_t)s2 * kAttnPart + 2 + d], num);
+  if (Sb <= 8) {  // every split's (m, l, o[d]) requested at once: one L2 round trip
+    float ms[8], ls[8], os[8];
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2)
+      if (s2 < Sb) {
+        ms[s2] = pp[(size_t)s2 * kAttnPart];
+        ls[s2] = pp[(size_t)s2 * kAttnPart + 1];
+        os[s2] = pp[(size_t)s2 * kAttnPart + 2 + d];
+      }
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2)
+      if (s2 < Sb) M = fmaxf(M, ms[s2]);
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2)
+      if (s2 < Sb) {
+        const float w = __expf(ms[s2] - M);
+        den = fmaf(w, ls[s2], den);
+        num = fmaf(w, os[s2], num);
+      }
+  } else {
+    for (int s2 = 0; s2 < Sb; ++s2) M = fmaxf(M, pp[(size_t)s2 * kAttnPart]);
+    for (int s2 = 0; s2 < Sb; ++s2) {
+      const float w = __expf(pp[(size_t)s2 * kAttnPart] - M);
+      den = fmaf(w, pp[(size_t)s2 * kAttnPart + 1], den);
+      num = fmaf(w, pp[(size_t)s2 * kAttnPart + 2 + d], num);
+    }
   }
   const __nv_bfloat16 ob = __float2bfloat16_rn(num / den);
   out[out_index(b, h * 128 + d, ld_out, out_np)] = __bfloat16_as_ushort(ob);
