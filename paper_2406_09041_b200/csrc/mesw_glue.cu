@@ -239,45 +239,75 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(
                  "l"(vb + t * kv_stride + c * 8) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
-  if (ROPE) pdl_wait();  // the new token's fused qkv row
   const uint16_t* qrow = q + (size_t)b * ld_q;
   if (ROPE) {
     const int p = L - 1;
     constexpr int half = D / 2;
-    for (int i = tid; i < G * half; i += kAttnThreads) {  // (head, pair) -> two rotated q values
-      const int hh = i / half, j = i % half;
-      const float inv = powf(theta, -2.0f * (float)j / (float)D);
-      float sn, cs;
-      sincosf((float)p * inv, &sn, &cs);
-      const uint16_t* v = qrow + (size_t)(g * G + hh) * D;
-      const float x0 = bf16_to_f32(v[j]), x1 = bf16_to_f32(v[j + half]);
-      qs[hh * D + j] = __bfloat162float(__float2bfloat16_rn(x0 * cs - x1 * sn)) * scale;
-      qs[hh * D + j + half] = __bfloat162float(__float2bfloat16_rn(x1 * cs + x0 * sn)) * scale;
+    constexpr int NQ = (G * half + kAttnThreads - 1) / kAttnThreads;  // (head, pair)s per thread
+    // the rotation angles depend only on the position: computed before the PDL wait, then
+    // every input element of the new row is requested at once (one round trip)
+    float qcs[NQ], qsn[NQ];
+#pragma unroll
+    for (int r = 0; r < NQ; ++r) {
+      const int i = tid + r * kAttnThreads, j = i % half;
+      qcs[r] = 1.f; qsn[r] = 0.f;
+      if (i < G * half) {
+        const float inv = powf(theta, -2.0f * (float)j / (float)D);
+        sincosf((float)p * inv, &qsn[r], &qcs[r]);
+      }
     }
-    if (n_cached < n) {  // this split holds the new position: rotate k, stage + append k / v
-      const int t = n - 1, n_heads = G * n_kv;
+    const bool new_row = n_cached < n;  // this split holds the new position: rotate k, stage + append k / v
+    float kcs = 1.f, ksn = 0.f;
+    if (new_row && tid < half) {
+      const float inv = powf(theta, -2.0f * (float)tid / (float)D);
+      sincosf((float)p * inv, &ksn, &kcs);
+    }
+    pdl_wait();  // the new token's fused qkv row
+    float x0[NQ], x1[NQ];
+#pragma unroll
+    for (int r = 0; r < NQ; ++r) {
+      const int i = tid + r * kAttnThreads, hh = i / half, j = i % half;
+      x0[r] = x1[r] = 0.f;
+      if (i < G * half) {
+        const uint16_t* v = qrow + (size_t)(g * G + hh) * D;
+        x0[r] = bf16_to_f32(v[j]);
+        x1[r] = bf16_to_f32(v[j + half]);
+      }
+    }
+    const int n_heads = G * n_kv;
+    uint16_t e0 = 0, e1 = 0;
+    if (new_row) {
+      const int j = tid < half ? tid : tid - half;
+      const uint16_t* v = qrow + (size_t)(tid < half ? n_heads + g : n_heads + n_kv + g) * D;
+      e0 = v[j];
+      e1 = v[j + half];
+    }
+#pragma unroll
+    for (int r = 0; r < NQ; ++r) {
+      const int i = tid + r * kAttnThreads, hh = i / half, j = i % half;
+      if (i < G * half) {
+        qs[hh * D + j] = __bfloat162float(__float2bfloat16_rn(x0[r] * qcs[r] - x1[r] * qsn[r])) * scale;
+        qs[hh * D + j + half] = __bfloat162float(__float2bfloat16_rn(x1[r] * qcs[r] + x0[r] * qsn[r])) * scale;
+      }
+    }
+    if (new_row) {
+      const int t = n - 1;
       const size_t cbase = (((size_t)b * ctx_max + p) * n_kv + g) * D;
       if (tid < half) {
         const int j = tid;
-        const float inv = powf(theta, -2.0f * (float)j / (float)D);
-        float sn, cs;
-        sincosf((float)p * inv, &sn, &cs);
-        const uint16_t* v = qrow + (size_t)(n_heads + g) * D;
-        const float x0 = bf16_to_f32(v[j]), x1 = bf16_to_f32(v[j + half]);
-        const uint16_t o0 = __bfloat16_as_ushort(__float2bfloat16_rn(x0 * cs - x1 * sn));
-        const uint16_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(x1 * cs + x0 * sn));
+        const float k0 = bf16_to_f32(e0), k1 = bf16_to_f32(e1);
+        const uint16_t o0 = __bfloat16_as_ushort(__float2bfloat16_rn(k0 * kcs - k1 * ksn));
+        const uint16_t o1 = __bfloat16_as_ushort(__float2bfloat16_rn(k1 * kcs + k0 * ksn));
         Ks[t * kAttnRow + j] = o0;
         Ks[t * kAttnRow + j + half] = o1;
         kc[cbase + j] = o0;
         kc[cbase + j + half] = o1;
       } else {
         const int j = tid - half;
-        const uint16_t* vv = qrow + (size_t)(n_heads + n_kv + g) * D;
-        const uint16_t v0 = vv[j], v1 = vv[j + half];
-        Vs[t * kAttnRow + j] = v0;
-        Vs[t * kAttnRow + j + half] = v1;
-        vc[cbase + j] = v0;
-        vc[cbase + j + half] = v1;
+        Vs[t * kAttnRow + j] = e0;
+        Vs[t * kAttnRow + j + half] = e1;
+        vc[cbase + j] = e0;
+        vc[cbase + j + half] = e1;
       }
     }
   } else {
