@@ -198,6 +198,17 @@ typedef struct {
    * Lets callers keep their own row order while the launch groups rows by expert
    * (mesw_pack_x_gather builds the grouped input).  NULL: row t -> row t. */
   const int32_t* y_rows;
+  /* Optional SwiGLU epilogue (the decode engine's fused gate|up linear): swiglu_I > 0 means
+   * columns [0, I) are gate and [I, 2I) up (n = 2I, I % 128 == 0, bf16 y, no row map /
+   * residual / activation).  Besides y, the launch writes act = silu(gate) * up (mesw_swiglu's
+   * arithmetic) in the canonical layout with act_np rows, and, when act_corr != NULL, its
+   * offset-code bias table act_corr[t * act_corr_ld + k-step].  counters must then hold
+   * n_pad/128 + I/128 entries (zero before first use, self-resetting). */
+  int32_t swiglu_I;
+  uint16_t* act;
+  int32_t act_np;
+  float* act_corr;
+  int32_t act_corr_ld;
 } mesw_linear_args;
 
 /* ------------------------------------------- K3: prefill fused multi-expert linear

@@ -37,7 +37,9 @@ class LinearArgs(C.Structure):
                 ("ldy", C.c_int32), ("residual", C.c_void_p), ("ld_res", C.c_int32),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
                 ("counters", C.c_void_p), ("num_ctas", C.c_int32), ("activation", C.c_int32),
-                ("x_corr", C.c_void_p), ("x_corr_ld", C.c_int32), ("y_rows", C.c_void_p)]
+                ("x_corr", C.c_void_p), ("x_corr_ld", C.c_int32), ("y_rows", C.c_void_p),
+                ("swiglu_I", C.c_int32), ("act", C.c_void_p), ("act_np", C.c_int32), ("act_corr", C.c_void_p),
+                ("act_corr_ld", C.c_int32)]
 
 
 class PrefillArgs(C.Structure):

@@ -28,7 +28,7 @@ int mesw_check_launch(const char* what) {
   return MESW_OK;
 }
 
-extern "C" int mesw_abi_version(void) { return 1; }
+extern "C" int mesw_abi_version(void) { return 2; }  // 2: mesw_linear_args gained the SwiGLU epilogue fields
 
 static int g_pdl = 1;
 int mesw_pdl_enabled() { return g_pdl; }

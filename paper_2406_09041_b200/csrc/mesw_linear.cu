@@ -120,6 +120,12 @@ struct LinearParams {
   int n_dq;   // delta issuers = active dequant groups (group g feeds delta issuer g)
   unsigned long long* tbuf;  // MESW_TIMING: per-CTA globaltimer stamps
   int dbg;  // reserved (MESW_DBG)
+  // SwiGLU epilogue (mesw_linear_args.swiglu_I): columns [0, I) gate, [I, 2I) up
+  int swiglu_I;
+  uint16_t* act;
+  int act_np;
+  float* act_corr;
+  int act_corr_ld;
 };
 
 struct Smem {
@@ -130,7 +136,7 @@ struct Smem {
   uint64_t accfull[2], accempty[2];
   uint64_t finbar;  // final-piece partials staged by bulk copy
   uint32_t tmem_base;
-  int flag;
+  int flag, sflag;
   struct { int on, cg, cgp, p_first, p_last, fast; } fin;  // final-piece reduction hand-off
   int tok2seg[kMaxRows];
   int half2seg[kMaxRows / 8];  // segment owning rows [8h, 8h + 8) (a segment begins on an 8-row half)
@@ -402,6 +408,61 @@ __device__ __forceinline__ void reduce_chunk(const LinearParams& p, const Smem& 
   }
   MESW_PROF(if (p.tbuf && threadIdx.x == 0) p.tbuf[4096 * 12 + (size_t)blockIdx.x * 8 + 1] = clock64();)
   epi_store16<YMAP, HALF>(p, S, cg, m, t0, vb, vd, fast, pre, dry);
+}
+
+// Offset-code bias weight of input k (mesw.h x_corr; same as mesw_glue.cu corr_w).
+__device__ __forceinline__ float act_corr_w(int k) {
+  const int l = ((k & 63) >> 1) & 7;
+  const int m = l < 6 ? l % 3 : l - 6;
+  return m == 0 ? 130.f : (m == 1 ? 34.f : 10.f);
+}
+
+// SwiGLU epilogue: called by the NT threads that just wrote the FINAL values of column group
+// cg (tid in [0, NT)).  Gate block b = cg (cg < I/128) and up block b = cg - I/128 are final
+// in two places of the launch; the second of them to finish computes act = silu(gate) * up
+// for block b -- mesw_swiglu's arithmetic -- from y (L2) and writes the canonical input of
+// the down projection plus its bias table (the SwiGLU launch disappears from the step).
+template <int NT>
+__device__ __forceinline__ void swiglu_final(const LinearParams& p, Smem& S, int cg, int tid) {
+  const int nb = p.swiglu_I >> 7;
+  const int blk = cg < nb ? cg : cg - nb;
+  if (blk < 0 || blk >= nb) return;
+  // the writers' y stores are ordered before thread 0's release by the barrier
+  // (cumulativity): one device-scope fence per CTA, not one per thread
+  if constexpr (NT == kThreads) __syncthreads(); else named_bar_sync(1, 128);
+  if (tid == 0) {
+    __threadfence();
+    const int prev = atomicAdd(&p.counters[p.n_cg + blk], 1);
+    S.sflag = prev == 1;
+    if (prev == 1) p.counters[p.n_cg + blk] = 0;  // self-reset for the next launch
+  }
+  if constexpr (NT == kThreads) __syncthreads(); else named_bar_sync(1, 128);
+  const bool second = S.sflag != 0;
+  if (!second) return;  // (thread 0's fence + atomic acquired the other half; the barrier passes it on)
+  const int I = p.swiglu_I, lane = tid & 31;
+  const int i = blk * 128 + 4 * lane;  // this lane's 4 consecutive channels of the block
+  for (int t = tid >> 5; t < p.B; t += NT / 32) {  // one warp per row
+    const uint16_t* r = reinterpret_cast<const uint16_t*>(p.y) + (size_t)t * p.ldy;
+    const uint2 g4 = __ldcg(reinterpret_cast<const uint2*>(r + i));
+    const uint2 u4 = __ldcg(reinterpret_cast<const uint2*>(r + I + i));
+    const uint32_t gg[2] = {g4.x, g4.y}, uu[2] = {u4.x, u4.y};
+    uint32_t o[2];
+    float c = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float g0 = bf16_lo(gg[h]), g1 = bf16_hi(gg[h]);
+      const float s0 = g0 / (1.f + __expf(-g0)), s1 = g1 / (1.f + __expf(-g1));
+      __nv_bfloat162 v = __floats2bfloat162_rn(s0 * bf16_lo(uu[h]), s1 * bf16_hi(uu[h]));
+      o[h] = *reinterpret_cast<uint32_t*>(&v);
+      c += act_corr_w(i + 2 * h) * (bf16_lo(o[h]) + bf16_hi(o[h]));
+    }
+    *reinterpret_cast<uint2*>(p.act + xc_index(t, i, p.act_np)) = make_uint2(o[0], o[1]);
+    if (p.act_corr) {
+#pragma unroll
+      for (int q = 16; q; q >>= 1) c += __shfl_xor_sync(0xffffffffu, c, q);
+      if (lane == 0) p.act_corr[(size_t)t * p.act_corr_ld + blk] = c;
+    }
+  }
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -880,6 +941,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
       if (gtid == 0 && pi == po.np - 1) MESW_STAMP(6);
       acc_use[ab]++;
       if (p.n_acc == 2) ab ^= 1;
+      if (whole && p.swiglu_I) swiglu_final<128>(p, S, cg, gtid);
       if (!whole) {
         named_bar_sync(1, 128);  // the partial stores above happen-before gtid 0's release
         // contributors to this column group: the pairs owning its first/last unit
@@ -909,6 +971,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
               reduce_chunk<YMAP, HALF>(p, S, cg, cgp, (int)rank, mrow, t0, p_first, p_last, fast, pre, nullptr);
             }
             if (gtid == 0) p.counters[cg] = 0;  // self-reset for the next launch
+            if (p.swiglu_I) swiglu_final<128>(p, S, cg, gtid);
           }
         }
       }
@@ -994,6 +1057,7 @@ __global__ void __launch_bounds__(kThreads, 1) me_linear_tc_kernel(const __grid_
     MESW_PROF(fp[3] = staged ? nC : -nC;)
     MESW_PROF(if (p.tbuf && threadIdx.x == 0) for (int i = 0; i < 4; ++i) p.tbuf[4096 * 40 + (size_t)blockIdx.x * 16 + i] = fp[i];)
     if (threadIdx.x == 0) p.counters[S.fin.cg] = 0;
+    if (p.swiglu_I) swiglu_final<kThreads>(p, S, fcg, threadIdx.x);
     if (threadIdx.x == 0) MESW_STAMP(4);
   }
   if (threadIdx.x == 0) MESW_STAMP2(5);
@@ -1102,6 +1166,15 @@ extern "C" int mesw_me_linear(const mesw_linear_args* a, void* stream) {
   p.activation = a->activation;
   p.x_corr = (a->n_segments > 0 && a->code_bits == 2) ? a->x_corr : nullptr;
   p.x_corr_ld = a->x_corr_ld;
+  p.swiglu_I = a->swiglu_I;
+  if (p.swiglu_I) {
+    if (p.swiglu_I < 0 || p.swiglu_I % kUnitN || 2 * p.swiglu_I != a->n || !a->y_bf16 || a->y_rows || !a->act ||
+        a->act_np < p.NP || a->act_np % 16 || (a->act_corr && a->act_corr_ld < p.swiglu_I / kUnitN) ||
+        a->residual || a->activation)
+      return mesw_fail(MESW_ERR_VALUE, "swiglu epilogue: n = 2 I (I % 128 == 0), bf16 y without row map / "
+                                       "residual / activation, act with >= canonical rows");
+    p.act = a->act; p.act_np = a->act_np; p.act_corr = a->act_corr; p.act_corr_ld = a->act_corr_ld;
+  }
   if (p.x_corr && p.x_corr_ld < p.n_ks)
     return mesw_fail(MESW_ERR_VALUE, "x_corr_ld must cover the k-steps of the linear");
   {

@@ -382,7 +382,9 @@ class LinearPlan:
     def __init__(self, xc: torch.Tensor, B: int, weight: DeviceWeight | None, table: ExpertTable | None,
                  segments, out: torch.Tensor, residual: torch.Tensor | None = None,
                  geom: LinearGeometry | None = None, num_ctas: int = 0, activation: str | None = None,
-                 x_corr: torch.Tensor | None = None, stream=None):
+                 x_corr: torch.Tensor | None = None, stream=None, swiglu: tuple | None = None):
+        """swiglu = (I, act, act_corr or None): the SwiGLU epilogue of mesw_linear_args (the
+        engine's gate|up linear writes the down projection's canonical input itself)."""
         L = _lib.lib()
         if geom is None:
             geom = weight.geom if weight is not None else next(
@@ -431,6 +433,14 @@ class LinearPlan:
                     or x_corr.shape[0] < canonical_rows(B) or x_corr.shape[1] < _ceil(geom.m) // 128):
                 raise ValueError("x_corr must be a contiguous f32 [canonical_rows(B), ceil(m/128)] tensor")
             a.x_corr, a.x_corr_ld = x_corr.data_ptr(), x_corr.stride(0)
+        if swiglu is not None:
+            I, act, act_corr = swiglu
+            a.swiglu_I, a.act, a.act_np = int(I), act.data_ptr(), canonical_rows(B)
+            if act.numel() < canonical_numel(B, int(I)):
+                raise ValueError("act too small for the canonical layout of B rows")
+            if act_corr is not None:
+                a.act_corr, a.act_corr_ld = act_corr.data_ptr(), act_corr.stride(0)
+            self.keep = self.keep + (act, act_corr)
         self.args = a
         self._fn = L.mesw_me_linear
 

@@ -27,6 +27,11 @@ from .synth import MistralShape
 
 # rope + KV-cache append run inside the attention launch (mesw_attention_decode_rope)
 _FUSED_ROPE = os.environ.get("MESW_ROPE_SPLIT") is None
+# SwiGLU in the gate|up launch's epilogue (mesw_linear_args.swiglu_I) saves one launch per
+# layer but lengthens the gate|up tail (the second finisher of each gate/up block pair reads
+# both halves back from L2): measured 6.13 vs 6.09 ms per C2 step, so it is opt-in
+# (MESW_SWIGLU_FUSED=1) and the separate mesw_swiglu launch stays the default.
+_FUSED_SWIGLU = os.environ.get("MESW_SWIGLU_FUSED") is not None
 
 PROJ_ORDER = ("q", "k", "v", "o", "gate", "up", "down")
 MAX_EXPERT_SLOTS = 128  # resident experts per engine (C5: 64 on one GPU)
@@ -368,7 +373,9 @@ class MistralMultiExpert:
                 tabs = self.tables[l]
                 layers.append(tuple(
                     LinearPlan(bufs[xin], rows, wsel(lw), tabs[ti] if segs else None, segs, out,
-                               residual=out if res else None, x_corr=bufs[xin + "_corr"], num_ctas=ctas[name])
+                               residual=out if res else None, x_corr=bufs[xin + "_corr"], num_ctas=ctas[name],
+                               swiglu=(s.intermediate, bufs["act"], bufs["act_corr"])
+                               if (name == "gu" and _FUSED_SWIGLU) else None)
                     for name, xin, wsel, ti, out, res in kinds))
             head = LinearPlan(bufs["xn"], rows, self.head, None, [], self.logits[r0:r1],
                               num_ctas=self._tuned_ctas("head", rows, [], bufs["xn"], None, self.head, None,
@@ -459,8 +466,9 @@ class MistralMultiExpert:
                 if trace:
                     trace("post", "gu", l, r0, r1, bufs)
             for (r0, r1, bufs, layers, _) in self._plans:
-                chk(L.mesw_swiglu(rows_ptr(self.gu, r0), self.gu.stride(0), r1 - r0, s.intermediate,
-                                  bufs["act"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "act"), st))
+                if not _FUSED_SWIGLU:  # (fused: the gate|up launch wrote act and its bias table)
+                    chk(L.mesw_swiglu(rows_ptr(self.gu, r0), self.gu.stride(0), r1 - r0, s.intermediate,
+                                      bufs["act"].data_ptr(), 0, canonical_rows(r1 - r0), *corr(bufs, "act"), st))
                 if trace:
                     trace("pre", "down", l, r0, r1, bufs)
                 layers[l][3](stream)

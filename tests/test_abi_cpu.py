@@ -27,7 +27,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), f"libmesw.so does not export {s}"
     assert sorted(_lib.SYMBOLS) == syms
-    assert L.mesw_abi_version() == 1
+    assert L.mesw_abi_version() == 2
 
 
 def test_packed_and_block_sizes():

@@ -304,3 +304,46 @@ def test_me_linear_caller_row_order_on_device():
     x2 = torch.flip(x, [0]).contiguous()
     xs.copy_(x2)
     assert torch.equal(g(), me_linear(x2, dw, table, segs, residual=res, out_dtype=torch.float32))
+
+
+def test_swiglu_epilogue_matches_swiglu_kernel():
+    """The fused gate|up launch with the SwiGLU epilogue (mesw_linear_args.swiglu_I) writes
+    the same act and bias table, bit for bit, as the plain launch followed by mesw_swiglu --
+    for stream-K splits (all SMs) and whole column groups (narrow grid)."""
+    import ctypes as C
+    import torch
+    from paper_2406_09041_b200 import _lib, compress
+    from paper_2406_09041_b200.device import (DeviceDelta, DeviceWeight, ExpertTable, LinearGeometry, LinearPlan,
+                                               canonical_numel, canonical_rows, corr_table, pack_x)
+    L = _lib.lib()
+    rng = np.random.default_rng(33)
+    m, I, B = 256, 512, 21
+    W = rng.normal(0, 0.05, size=(m, 2 * I)).astype(np.float32)
+    geom = LinearGeometry(m, (2 * I,))
+    dw = DeviceWeight.from_dense([W])
+    table = ExpertTable("cuda")
+    man = {"model_id": "x", "domain": "d", "base_digest": "0", "layer_count": 1}
+    for e in range(2):
+        ol = om.random_layer(rng, m, 2 * I, 2, 8)
+        table.set(e, DeviceDelta.from_blocks([compress.deserialize_artifact(om.serialize_artifact(man, [ol])).layers[0]]))
+    x = torch.from_numpy(rng.normal(0, 1, size=(B, m)).astype(np.float32)).to(torch.bfloat16).cuda()
+    corr = corr_table(B, m, "cuda")
+    xc = pack_x(x, corr=corr)
+    segs = [(0, 5, 0), (8, 21, 1)]
+    s = torch.cuda.current_stream()
+    for ctas in (0, 8):
+        gu1 = torch.empty((B, 2 * I), dtype=torch.bfloat16, device="cuda")
+        gu2 = torch.empty_like(gu1)
+        act1 = torch.zeros(canonical_numel(B, I), dtype=torch.bfloat16, device="cuda")
+        act2 = torch.zeros_like(act1)
+        c1, c2 = corr_table(B, I, "cuda"), corr_table(B, I, "cuda")
+        LinearPlan(xc, B, dw, table, segs, gu1, geom=geom, x_corr=corr, num_ctas=ctas)()
+        _lib.check(L.mesw_swiglu(gu1.data_ptr(), gu1.stride(0), B, I, act1.data_ptr(), 0, canonical_rows(B),
+                                 c1.data_ptr(), c1.stride(0), C.c_void_p(s.cuda_stream)))
+        for _ in range(2):  # second launch: the block counters reset themselves
+            LinearPlan(xc, B, dw, table, segs, gu2, geom=geom, x_corr=corr, num_ctas=ctas,
+                       swiglu=(I, act2, c2))()
+        torch.cuda.synchronize()
+        assert torch.equal(gu1, gu2)
+        assert torch.equal(act1, act2)
+        assert torch.equal(c1, c2)
