@@ -72,3 +72,39 @@ def test_batched_multi_model_forward_gpu():
     for a, b in zip(out, out2[::-1]):
         if a[1] is not None:
             assert np.array_equal(a[1], b[1])
+
+
+def _reference_toylm():
+    """The unmodified reference package installed by tools/install_reference.sh into
+    baseline/_ref (git-ignored; it travels to the GPU box with the repo), or None."""
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "meswitch")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from meswitch import toylm
+    return toylm
+
+
+def test_gpu_providers_in_the_reference_packages_own_forward():
+    """The drop-in proper: the reference package's OWN toylm.forward_with_delta and
+    greedy_decode (toylm.py:189-248) call the GPU providers through their protocol
+    (matvec_batch / rows) and reproduce the reference-made golden outputs."""
+    toylm = _reference_toylm()
+    if toylm is None:
+        pytest.skip("reference package not installed (tools/install_reference.sh)")
+    from paper_2406_09041_b200 import compress
+    from paper_2406_09041_b200.infer import GpuCompressedProvider
+    zb = np.load(os.path.join(GOLDEN, "toy_base.npz"))
+    layers = tuple(zb[f"layer{i}"] for i in range(4))
+    model = toylm.ToyLM(vocab=zb["embedding"].shape[0], width=zb["embedding"].shape[1], depth=len(layers),
+                        embedding=zb["embedding"], layers=layers, head=zb["head"])
+    ze = np.load(os.path.join(GOLDEN, "toy_expected.npz"))
+    for e in range(3):
+        art = compress.load_artifact(os.path.join(GOLDEN, f"toy_expert_{e}.mesw"))
+        provs = [GpuCompressedProvider(l) for l in art.layers]
+        logits = toylm.forward_with_delta(model, provs, ze["tokens"])
+        ref = ze[f"fwd_delta_{e}"]
+        assert np.max(np.abs(logits - ref)) <= 1e-4 * np.max(np.abs(ref))  # SPEC.md:373 (1e-4)
+        assert toylm.greedy_decode(model, ze["prompt"], 12, provs) == ze[f"greedy_{e}"].tolist()
